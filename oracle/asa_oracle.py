@@ -1,0 +1,466 @@
+"""Plain fp64 CPU oracle for the ASA forward hot path (BLADE, arXiv 2508.10774).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import or call
+anything in ``oracle/``.  The product path (``paper_2508_10774_b200``) never
+imports it and shares no code with it: no kernels, headers, helpers, tables or
+constants.  The only thing both sides consume is the seeded input data made by
+``paper_2508_10774_b200/inputs.py`` (which contains none of the method's
+arithmetic).
+
+Everything here follows the paper step by step, in its order and notation,
+and is deliberately slow and unblocked.  Citations use ``P:<line>`` for
+``PAPER.md`` lines and name the algorithm line; ``DESIGN.md §Readings`` lists
+every reading taken where the paper is silent (R-1 ... R-16, mirroring
+SURVEY §8(c) C-1 ... C-16).
+
+Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
+  * sampler          - public splitmix64 outputs; survey KATs (tests/golden);
+                       chi^2 uniformity; order-statistics rank law P:450-454.
+  * probe (A4-A6)    - torch.softmax + torch max_pool2d on the sampled logits
+                       (library routines); k=b exhaustive probe == dense
+                       importance map P:117; uniform-logit factor b/k P:479;
+                       Alg. 3 streaming form == two-pass form.
+  * selection (A7-8) - SPEC worked examples; brute-force m0 with math.fsum;
+                       numpy lexsort top-m; power-of-two scale invariance;
+                       tau monotonicity; clamp safety.
+  * attention (A9)   - torch scaled_dot_product_attention (fp64) with the
+                       block mask expanded to a boolean token mask; LSE vs
+                       torch.logsumexp; V=1 => O=1; V=0 => O=0; V=I => O=P.
+Every function of this module has at least one pin; none is "parity unpinned"
+except the end-to-end composition sample -> probe -> select, which the paper
+gives no worked example for.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# ---------------------------------------------------------------------------
+# A1  block partition (Alg.1 l.2 "Partition Q, K into N_b = N/b blocks";
+#     P:627 Alg.2 l.1 "Make length divisible by b: Pad").  Reading R-8: the pad
+#     is logical; padded rows never enter sampling, softmax or attention.
+# ---------------------------------------------------------------------------
+
+
+def num_blocks(N: int, b: int) -> int:
+    """N_b = ceil(N / b)  (T_r = ceil(S/b))."""
+    return (N + b - 1) // b
+
+
+def block_valid(N: int, b: int, i: int) -> int:
+    """Number of real (un-padded) rows of block i."""
+    return min(b, N - i * b)
+
+
+def block_samples(N: int, b: int, k: int, i: int) -> int:
+    """k_i = min(k, valid_i): a trailing block with fewer than k real rows
+    contributes all of them (reading R-8)."""
+    return min(k, block_valid(N, b, i))
+
+
+# ---------------------------------------------------------------------------
+# A2  random sampling of k tokens per block ("we sample k representative
+#     tokens"; Alg.1 l.3 "Randomly sample k tokens from each block";
+#     P:628-629 Alg.2 BlockSample).  The paper names no generator; reading R-1
+#     fixes a counter-based hash so both implementations can replay it.
+# ---------------------------------------------------------------------------
+
+_M64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+
+
+def fmix64(z: int) -> int:
+    """splitmix64 output finaliser (xor-shift 30, *0xBF58476D1CE4E5B9,
+    xor-shift 27, *0x94D049BB133111EB, xor-shift 31), mod 2^64."""
+    z &= _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def sm(x: int, n: int) -> int:
+    """sm(x, n) = fmix64(x + G*(n+1)): the n-th splitmix64 output of state x."""
+    return fmix64((x + _GOLDEN * (n + 1)) & _M64)
+
+
+def sample_key(seed: int, u: int, i: int, which: int) -> int:
+    """Per-(unit, block, Q-or-K) stream key (reading R-1)."""
+    return sm(sm(sm(seed & _M64, u), i), which)
+
+
+def sample_offsets(seed: int, u: int, i: int, which: int, valid: int, k: int,
+                   mode: int = 0) -> list[int]:
+    """The in-block offsets sampled for block i of unit u, ascending.
+
+    mode 0 (default, reading R-1): k_i = min(k, valid) distinct offsets,
+      uniform without replacement: rank every offset o in [0, valid) by the
+      pair (sm(key, o), o) and keep the k_i smallest.
+    mode 1 (strided ablation): o_j = floor((2j+1)*valid/(2*k_i)).
+    """
+    k_i = min(k, valid)
+    if mode == 1:
+        return [((2 * j + 1) * valid) // (2 * k_i) for j in range(k_i)]
+    if mode != 0:
+        raise ValueError("mode must be 0 or 1 (mode 2 = caller-supplied)")
+    key = sample_key(seed, u, i, which)
+    ranked = sorted((sm(key, o), o) for o in range(valid))
+    return sorted(o for _, o in ranked[:k_i])
+
+
+# ---------------------------------------------------------------------------
+# Parameters
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class AsaParams:
+    """The ABI parameter block, in plain Python (reading R-5/R-6 for tau and
+    the clamps: integer keep_min/keep_max per row)."""
+
+    block: int = 128          # b
+    samples: int = 16         # k
+    tau: float = 0.9          # threshold
+    keep_min: int = 1         # lo           ("clamp m")
+    keep_max: int = 1 << 30   # hi, clipped to N_b
+    scale: float | None = None  # softmax scale; default fp32(1/sqrt(d)) (R-3)
+    seed: int = 42            # P:603 Table 7 "Seed 42"
+    sample_mode: int = 0      # 0 hash-random, 1 strided, 2 supplied
+    share_qk: bool = False    # same offsets for Q and K
+    unit_offset: int = 0      # global index of the first unit (sharding)
+
+
+def default_scale(d: int) -> float:
+    """fp32(1/sqrt(d)) widened to fp64 (reading R-3, "/ sqrt(d)")."""
+    return float(np.float32(1.0 / math.sqrt(d)))
+
+
+# ---------------------------------------------------------------------------
+# A3-A6  probe: sampled attention and max-pool (Alg.1 l.4-5)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class UnitSamples:
+    """Sampled row indices of one unit, block-major, ascending in each block."""
+
+    rows_q: np.ndarray          # [N_k] absolute row index of each sampled query
+    rows_k: np.ndarray          # [N_k] absolute row index of each sampled key
+    blk_q: np.ndarray           # [N_k] block id of each sampled query row
+    blk_k: np.ndarray           # [N_k] block id of each sampled key
+    offsets_q: list = field(default_factory=list)   # per block, in-block offsets
+    offsets_k: list = field(default_factory=list)
+
+
+def draw_samples(N: int, p: AsaParams, u_global: int,
+                 supplied: np.ndarray | None = None) -> UnitSamples:
+    """BlockSample(Q_p, b, k) and BlockSample(K_p, b, k).
+
+    ``supplied`` (mode 2) is an int array [2, N_b, k] of in-block offsets,
+    -1 padded, [0] for Q and [1] for K."""
+    b, k = p.block, p.samples
+    Nb = num_blocks(N, b)
+    oq, ok = [], []
+    for i in range(Nb):
+        valid = block_valid(N, b, i)
+        if p.sample_mode == 2:
+            k_i = block_samples(N, b, k, i)
+            oq.append(sorted(int(x) for x in supplied[0, i, :k_i]))
+            ok.append(sorted(int(x) for x in supplied[1, i, :k_i]))
+        else:
+            oq.append(sample_offsets(p.seed, u_global, i, 0, valid, k, p.sample_mode))
+            ok.append(sample_offsets(p.seed, u_global, i, 0 if p.share_qk else 1,
+                                     valid, k, p.sample_mode))
+    rows_q = np.array([i * b + o for i in range(Nb) for o in oq[i]], dtype=np.int64)
+    rows_k = np.array([i * b + o for i in range(Nb) for o in ok[i]], dtype=np.int64)
+    blk_q = np.array([i for i in range(Nb) for _ in oq[i]], dtype=np.int64)
+    blk_k = np.array([i for i in range(Nb) for _ in ok[i]], dtype=np.int64)
+    return UnitSamples(rows_q, rows_k, blk_q, blk_k, oq, ok)
+
+
+def row_softmax(L: np.ndarray) -> np.ndarray:
+    """softmax over each row with the row max subtracted, fp64."""
+    m = L.max(axis=1, keepdims=True)
+    E = np.exp(L - m)
+    return E / E.sum(axis=1, keepdims=True)
+
+
+def probe_pimp(q_u: np.ndarray, k_u: np.ndarray, s: UnitSamples, Nb: int,
+               scale: float) -> np.ndarray:
+    """P_imp of one unit, two-pass definition.
+
+    A3  Q_s, K_s = the sampled rows, block-major              (Alg.1 l.3)
+    A4  L = Q_s K_s^T * scale  (fp64; bf16 products are exact) (Alg.1 l.4)
+    A5  P~ = softmax(L) over all N_k sampled keys (reading R-2)
+    A6  P_imp[i, j] = max over the k_i x k_j sub-block of P~   (Alg.1 l.5)
+    """
+    Qs = q_u[s.rows_q].astype(np.float64)
+    Ks = k_u[s.rows_k].astype(np.float64)
+    L = (Qs @ Ks.T) * scale
+    Pt = row_softmax(L)
+    # sampled rows are block-major, so block i owns one contiguous run of
+    # rows (and block j one run of columns); every block has k_i >= 1 rows.
+    q_starts = np.searchsorted(s.blk_q, np.arange(Nb))
+    k_starts = np.searchsorted(s.blk_k, np.arange(Nb))
+    row_max = np.maximum.reduceat(Pt, q_starts, axis=0)        # [Nb, N_k]
+    return np.maximum.reduceat(row_max, k_starts, axis=1)      # [Nb, Nb]
+
+
+def probe_pimp_streaming(q_u: np.ndarray, k_u: np.ndarray, s: UnitSamples,
+                         Nb: int, scale: float) -> np.ndarray:
+    """The same P_imp by Alg. 3 GetMaxPooledAttnMap, literally:
+    running max M~, running sum l~, stash R~[:, j] = m_ij, then
+    A[i, j] = max(e^{R~[:, j] - M~} / l~).  Used only to pin probe_pimp."""
+    Qs = q_u[s.rows_q].astype(np.float64)
+    Ks = k_u[s.rows_k].astype(np.float64)
+    A = np.zeros((Nb, Nb), dtype=np.float64)
+    for i in range(Nb):                                   # l.6
+        Qi = Qs[s.blk_q == i]
+        M = np.full(Qi.shape[0], -np.inf)                 # l.7  M~
+        ell = np.zeros(Qi.shape[0])                       # l.8  l~
+        R = np.full((Qi.shape[0], Nb), -np.inf)           # l.9  R~
+        for j in range(Nb):                               # l.10
+            Kj = Ks[s.blk_k == j]
+            s_ij = (Qi @ Kj.T) * scale                    # l.11
+            m_ij = s_ij.max(axis=1)                       # l.12
+            P_ij = np.exp(s_ij - m_ij[:, None])
+            l_ij = P_ij.sum(axis=1)                       # l.13
+            m_new = np.maximum(M, m_ij)
+            ell = np.exp(M - m_new) * ell + np.exp(m_ij - m_new) * l_ij  # l.14
+            M = m_new                                     # l.15
+            R[:, j] = m_ij
+        for j in range(Nb):                               # l.17
+            A[i, j] = (np.exp(R[:, j] - M) / ell).max()   # l.18-19
+    return A
+
+
+def dense_importance_map(q_u: np.ndarray, k_u: np.ndarray, b: int,
+                         scale: float) -> np.ndarray:
+    """The conceptual full importance: P = softmax(Q K^T / sqrt(d))
+    over all N keys, then b x b max-pooling.  Only a test aid (pins the probe
+    via k = b, P:117 vs P:146-147)."""
+    N = q_u.shape[0]
+    Nb = num_blocks(N, b)
+    P = row_softmax((q_u.astype(np.float64) @ k_u.astype(np.float64).T) * scale)
+    out = np.zeros((Nb, Nb))
+    for i in range(Nb):
+        for j in range(Nb):
+            out[i, j] = P[i * b:(i + 1) * b, j * b:(j + 1) * b].max()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# A7-A8  selection and compaction (Alg.1 l.6-11)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class RowSelection:
+    phat: np.ndarray      # normalised row
+    order: list           # block ids, p-hat descending, ties by ascending id
+    csum: list            # C_m for m = 1..N_b, sequential fp64 sums
+    m0: int               # smallest m with C_m >= tau, else N_b
+    m: int                # clamp(m0, lo, hi)
+    kept: list            # kept block ids, ascending
+
+
+def select_row(p_row: np.ndarray, tau: float, lo: int, hi: int) -> RowSelection:
+    """One row of Alg. 1 l.7-10.
+
+    l.7  p~_j = P_imp(i, j) / sum_k P_imp(i, k)   (sum ascending j, fp64)
+    l.8  sort descending (reading R-7: ties -> lower block id first)
+    l.9  smallest m with sum_{r<=m} s_r >= tau (reading R-4: '>=', Alg. 1,
+         not 'exceed' of P:124; if never reached, m0 = N_b), then clamp m to
+         [lo, hi] (reading R-6: integer clamps)
+    l.10 M[i, j] = 1 for the top m indices.
+    """
+    Nb = len(p_row)
+    Z = 0.0
+    for j in range(Nb):
+        Z += float(p_row[j])
+    phat = np.array([float(p_row[j]) / Z for j in range(Nb)])
+    order = sorted(range(Nb), key=lambda j: (-phat[j], j))
+    csum, c = [], 0.0
+    for j in order:
+        c += phat[j]
+        csum.append(c)
+    m0 = Nb
+    for r in range(Nb):
+        if csum[r] >= tau:
+            m0 = r + 1
+            break
+    m = min(max(m0, lo), hi)
+    return RowSelection(phat, order, csum, m0, m, sorted(order[:m]))
+
+
+def clamp_bounds(Nb: int, p: AsaParams) -> tuple[int, int]:
+    lo = max(1, min(p.keep_min, Nb))
+    hi = max(lo, min(p.keep_max, Nb))
+    return lo, hi
+
+
+# ---------------------------------------------------------------------------
+# Whole-unit and batched drivers
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class MaskResult:
+    mask: np.ndarray        # [BH, N_b, N_b] uint8
+    kv_idx: np.ndarray      # [BH, N_b, N_b] int32, kept ascending, -1 tail
+    kv_cnt: np.ndarray      # [BH, N_b] int32
+    p_imp: np.ndarray       # [BH, N_b, N_b] fp64 raw max-pooled P_imp
+    sample_idx: np.ndarray  # [BH, 2, N_b, k] int32 in-block offsets, -1 pad
+    rows: list              # [BH][N_b] RowSelection
+
+
+def to_f64(x) -> np.ndarray:
+    """Widen bf16/fp32 torch or numpy data to fp64 exactly."""
+    if hasattr(x, "detach"):
+        x = x.detach().float().cpu().numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def asa_mask(q, k, p: AsaParams, supplied_samples: np.ndarray | None = None,
+             units: list | None = None) -> MaskResult:
+    """Alg. 1 with Alg. 2/3 as the definition of
+    P_imp, for every unit of q, k of shape [BH, N, d] (any float type;
+    widened to fp64).  ``units`` restricts the work to a subset of local
+    units (others are left zero / -1)."""
+    q = to_f64(q)
+    k = to_f64(k)
+    BH, N, d = q.shape
+    b, ks = p.block, p.samples
+    Nb = num_blocks(N, b)
+    scale = default_scale(d) if p.scale is None else float(p.scale)
+    lo, hi = clamp_bounds(Nb, p)
+    mask = np.zeros((BH, Nb, Nb), dtype=np.uint8)
+    kv_idx = np.full((BH, Nb, Nb), -1, dtype=np.int32)
+    kv_cnt = np.zeros((BH, Nb), dtype=np.int32)
+    p_imp = np.zeros((BH, Nb, Nb), dtype=np.float64)
+    sidx = np.full((BH, 2, Nb, ks), -1, dtype=np.int32)
+    rows = [[None] * Nb for _ in range(BH)]
+    for u in (range(BH) if units is None else units):
+        sup = None if supplied_samples is None else supplied_samples[u]
+        s = draw_samples(N, p, p.unit_offset + u, sup)
+        for i in range(Nb):
+            sidx[u, 0, i, :len(s.offsets_q[i])] = s.offsets_q[i]
+            sidx[u, 1, i, :len(s.offsets_k[i])] = s.offsets_k[i]
+        P = probe_pimp(q[u], k[u], s, Nb, scale)
+        p_imp[u] = P
+        for i in range(Nb):
+            sel = select_row(P[i], float(p.tau), lo, hi)
+            rows[u][i] = sel
+            mask[u, i, sel.kept] = 1
+            kv_idx[u, i, :sel.m] = sel.kept
+            kv_cnt[u, i] = sel.m
+    return MaskResult(mask, kv_idx, kv_cnt, p_imp, sidx, rows)
+
+
+# ---------------------------------------------------------------------------
+# A9  block-sparse attention ("binary sparse mask M is directly
+#     integrated with a block-sparse attention kernel"); LSE by reading R-10.
+# ---------------------------------------------------------------------------
+
+
+def sparse_attention_unit(q_u, k_u, v_u, kv_idx_u, kv_cnt_u, b: int,
+                          scale: float, qblocks=None):
+    """For each query row r of q-block i:
+        T     = union over kept j of [j*b, min((j+1)*b, N))
+        LSE_r = ln sum_{t in T} exp(scale * q_r . k_t)
+        O_r   = sum_{t in T} exp(scale * q_r . k_t - LSE_r) v_t
+    in fp64.  Returns (O [N, d] fp64, LSE [N] fp64); rows of q-blocks not in
+    ``qblocks`` are NaN."""
+    q_u, k_u, v_u = to_f64(q_u), to_f64(k_u), to_f64(v_u)
+    N, d = q_u.shape
+    Nb = num_blocks(N, b)
+    O = np.full((N, v_u.shape[1]), np.nan)
+    LSE = np.full(N, np.nan)
+    for i in (range(Nb) if qblocks is None else qblocks):
+        r0, r1 = i * b, min((i + 1) * b, N)
+        cols = np.concatenate([np.arange(j * b, min((j + 1) * b, N))
+                               for j in kv_idx_u[i, :kv_cnt_u[i]]])
+        S = (q_u[r0:r1] @ k_u[cols].T) * scale
+        mx = S.max(axis=1, keepdims=True)
+        E = np.exp(S - mx)
+        ell = E.sum(axis=1, keepdims=True)
+        O[r0:r1] = (E @ v_u[cols]) / ell
+        LSE[r0:r1] = (mx + np.log(ell))[:, 0]
+    return O, LSE
+
+
+def sparse_attention(q, k, v, kv_idx, kv_cnt, b: int, scale: float | None = None,
+                     units=None, qblocks=None):
+    """A9 for [BH, N, d] inputs; returns fp64 O [BH, N, d], LSE [BH, N]."""
+    q, k, v = to_f64(q), to_f64(k), to_f64(v)
+    BH, N, d = q.shape
+    scale = default_scale(d) if scale is None else float(scale)
+    O = np.full(q.shape[:2] + (v.shape[2],), np.nan)
+    LSE = np.full((BH, N), np.nan)
+    for u in (range(BH) if units is None else units):
+        O[u], LSE[u] = sparse_attention_unit(q[u], k[u], v[u], kv_idx[u],
+                                             kv_cnt[u], b, scale, qblocks)
+    return O, LSE
+
+
+# ---------------------------------------------------------------------------
+# Tie band (operational form of BASELINE.json's "bit-exact except where a
+# block score lies within 1e-6 relative of the selection threshold"; reading
+# R-14 / DESIGN.md §Tie band).
+# ---------------------------------------------------------------------------
+
+
+def tie_exemption(sel: RowSelection, tau: float, lo: int, hi: int,
+                  eps: float = 1e-6) -> dict:
+    """Classify one oracle row.  Returns {'exempt': bool, 'counts': set of
+    accepted kv_cnt values, 'pivot_lo': p-hat lower bound for kept blocks,
+    'pivot_hi': p-hat upper bound for dropped blocks}.
+
+    T1 (cut ambiguity): |C_m' - tau| <= eps*tau for m' in {m0-1, m0} and the
+        clamped count would change with the cut.
+    T2 (membership ambiguity): m < N_b and p_(m) - p_(m+1) <= eps * p_(m).
+    """
+    Nb = len(sel.order)
+    clamp = lambda x: min(max(x, lo), hi)
+    counts = {sel.m}
+    t1 = False
+    for mp in (sel.m0 - 1, sel.m0):
+        if 1 <= mp <= Nb and abs(sel.csum[mp - 1] - tau) <= eps * tau:
+            for alt in (mp, mp + 1):
+                if 1 <= alt <= Nb and clamp(alt) != sel.m:
+                    counts.add(clamp(alt))
+                    t1 = True
+    sorted_p = [sel.phat[j] for j in sel.order]
+    t2 = False
+    for mm in counts:
+        if mm < Nb and sorted_p[mm - 1] - sorted_p[mm] <= eps * sorted_p[mm - 1]:
+            t2 = True
+    return {"exempt": t1 or t2, "t1": t1, "t2": t2, "counts": counts,
+            "sorted_p": sorted_p}
+
+
+def check_row_against(sel: RowSelection, tau: float, lo: int, hi: int,
+                      got_kept: list, eps: float = 1e-6) -> str | None:
+    """Return None if a device row (its kept block ids) is acceptable for the
+    oracle row ``sel`` under the tie band, else a reason string."""
+    got_kept = sorted(int(j) for j in got_kept)
+    if got_kept == sel.kept:
+        return None
+    te = tie_exemption(sel, tau, lo, hi, eps)
+    if not te["exempt"]:
+        return f"mismatch outside tie band: want {sel.kept} got {got_kept}"
+    mm = len(got_kept)
+    if mm not in te["counts"]:
+        return f"count {mm} not in accepted {sorted(te['counts'])}"
+    pivot = te["sorted_p"][mm - 1]
+    kept = set(got_kept)
+    for j in range(len(sel.phat)):
+        pj = sel.phat[j]
+        if j in kept and pj < (1 - eps) * pivot:
+            return f"kept block {j} p={pj} below pivot {pivot}"
+        if j not in kept and pj > (1 + eps) * pivot:
+            return f"dropped block {j} p={pj} above pivot {pivot}"
+    return None
