@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native ASA forward (BLADE, arXiv 2508.10774).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl blade|reference]
+                    [--workload wan|cog|tiny] [--keep 51 | --tau-mode] [--attn auto|tcgen05|mma]
+
+One STEP = one pass of the whole hot path (mask
+generation, then block-sparse attention) over one batch: at N=1 the
+Wan2.1-1.3B single attention layer of BASELINE.json configs[1]
+(B=1, H=12, N=32760, d=128, bf16, smooth-field synthetic inputs,
+keep-ratio 51/256 = sparsity 0.801 by default).  At N GPUs the batch is N
+samples (units sharded by (batch, head), one sample per rank, no collective
+on the data path): "scaling": "weak".
+
+metric  = BASELINE.json metric: active-block TFLOP/s of the whole ASA call
+          (active FLOP = 4 d sum over kept (i,j) valid_i valid_j, probe FLOP
+          excluded) and ms per call; value = all ranks' active FLOP / max
+          over ranks of the device time.
+e2e     = the same metric through the C ABI with host buffers: pinned host
+          Q/K/V -> device, ASA forward, O + LSE -> pinned host, every step.
+roofline = attention kernel (the dominant kernel) against the measured bf16
+          peak in MEASURED_PEAKS.json.
+cpu_baseline = the fp64 oracle (oracle/) on a bounded sample, rank 0, N=1.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2508_10774_b200 import inputs  # noqa: E402
+
+METRIC = "ASA fwd ms/call and effective TFLOPS (active blocks) vs bf16 peak at 1/2/4/8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
+    ap.add_argument("--workload", default="wan", choices=["wan", "cog", "tiny"])
+    ap.add_argument("--keep", type=int, default=None,
+                    help="keep-ratio mode: lo = hi = KEEP blocks per row (default 51 wan / 25 cog)")
+    ap.add_argument("--tau-mode", action="store_true", help="pure tau mode (lo=ceil(.05 Nb), hi=Nb)")
+    ap.add_argument("--tau", type=float, default=0.9)
+    ap.add_argument("--attn", default="auto", choices=["auto", "tcgen05", "mma"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def mask_params(w, args, Nb):
+    if args.tau_mode:
+        return dict(tau=args.tau, keep_min=max(1, -(-5 * Nb // 100)), keep_max=Nb), "tau"
+    keep = args.keep if args.keep is not None else {"wan": 51, "cog": 25, "tiny": 2}[args.workload]
+    keep = min(keep, Nb)
+    return dict(tau=args.tau, keep_min=keep, keep_max=keep), f"keep{keep}"
+
+
+def active_flop(kv_idx: np.ndarray, kv_cnt: np.ndarray, N: int, d: int, b: int = 128) -> float:
+    """4 d sum_{u, kept (i, j)} valid_i valid_j."""
+    Nb = kv_cnt.shape[1]
+    valid = np.array([min(b, N - i * b) for i in range(Nb)], dtype=np.float64)
+    total = 0.0
+    for u in range(kv_cnt.shape[0]):
+        for i in range(Nb):
+            idx = kv_idx[u, i, :kv_cnt[u, i]]
+            total += valid[i] * valid[idx].sum()
+    return 4.0 * d * total
+
+
+def probe_flop(BH, N, d, k=16, b=128):
+    Nb = (N + b - 1) // b
+    nk = sum(min(k, min(b, N - i * b)) for i in range(Nb))
+    return 2.0 * BH * nk * nk * d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.count(",") >= 7]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit()),
+                "samples": len(rows), "reasons": reasons}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except (OSError, ValueError):
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def traffic_for(workload: str, kernel: str):
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t.get(workload, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle legs (the only place bench.py touches oracle/)
+# ---------------------------------------------------------------------------
+
+
+def oracle_sample(q, k, v, w, mp, qblocks: int):
+    """Time the fp64 oracle on one unit: full mask, attention on `qblocks`
+    evenly spaced query blocks; returns (active FLOP of the whole unit,
+    estimated seconds for the whole unit, description)."""
+    from oracle import asa_oracle as O
+    p = O.AsaParams(tau=mp["tau"], keep_min=mp["keep_min"], keep_max=mp["keep_max"])
+    t0 = time.perf_counter()
+    r = O.asa_mask(q[:1], k[:1], p)
+    t_mask = time.perf_counter() - t0
+    Nb = r.kv_cnt.shape[1]
+    blocks = sorted(set(np.linspace(0, Nb - 1, qblocks).astype(int).tolist()))
+    t0 = time.perf_counter()
+    O.sparse_attention(q[:1], k[:1], v[:1], r.kv_idx, r.kv_cnt, 128, qblocks=blocks)
+    t_att = time.perf_counter() - t0
+    flop = active_flop(r.kv_idx, r.kv_cnt, w.N, w.d)
+    sample_flop = 4.0 * w.d * sum(min(128, w.N - i * 128) * sum(
+        min(128, w.N - j * 128) for j in r.kv_idx[0, i, :r.kv_cnt[0, i]]) for i in blocks)
+    est = t_mask + t_att * flop / max(sample_flop, 1.0)
+    desc = (f"1 of {w.B * w.H} units: full mask ({t_mask:.1f} s) + attention on {len(blocks)} of "
+            f"{Nb} query blocks ({t_att:.1f} s), scaled by active FLOP to the unit")
+    return flop, est, desc
+
+
+def cores_used() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the oracle as it stands, on bounded samples."""
+    if rank != 0:
+        return
+    w = inputs.WORKLOADS[args.workload]
+    q, k, v = inputs.smooth(1, 1, w.N, w.d, w.grid, w.n_text, w.ell, w.beta, w.sigma_n, seed=42)
+    Nb = (w.N + 127) // 128
+    mp, mode = mask_params(w, args, Nb)
+    qb = 4 if args.workload != "tiny" else Nb
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm state worth discarding beyond the first sample
+    vals, secs = [], []
+    desc = ""
+    for _ in range(args.steps):
+        flop, est, desc = oracle_sample(q, k, v, w, mp, qb)
+        vals.append(flop / est / 1e12)
+        secs.append(est)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(secs) * 1e3 * w.B * w.H, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d, "mask": mode,
+                   "tau": mp["tau"], "sample_per_step": desc},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores_used(),
+                         "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# CUDA path
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2508_10774_b200 import asa as A
+
+    w = inputs.WORKLOADS[args.workload]
+    # weak scaling: one sample (H units) per rank; rank r = sample r, units [rH, rH + H)
+    q_h, k_h, v_h = inputs.smooth(1, w.H, w.N, w.d, w.grid, w.n_text, w.ell, w.beta, w.sigma_n,
+                                  seed=42 + rank)
+    BH, N, d = q_h.shape
+    Nb = (N + 127) // 128
+    mp, mode = mask_params(w, args, Nb)
+    impl = {"auto": A.ATTN_AUTO, "tcgen05": A.ATTN_TCGEN05, "mma": A.ATTN_MMA_SYNC}[args.attn]
+    q, k, v = (t.to(dev) for t in (q_h, k_h, v_h))
+    stream = torch.cuda.current_stream()
+    unit_offset = rank * w.H
+
+    def step():
+        m = A.blade_asa_mask(q, k, unit_offset=unit_offset, want_mask=False, **mp)
+        ev_mid.record(stream)
+        A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl)
+        return m
+
+    ev_mid = torch.cuda.Event(enable_timing=True)
+    for _ in range(max(args.warmup, 3)):
+        m = step()
+    torch.cuda.synchronize()
+    kv_idx_np, kv_cnt_np = m.kv_idx.cpu().numpy(), m.kv_cnt.cpu().numpy()
+    flop = active_flop(kv_idx_np, kv_cnt_np, N, d)
+    refined = int(m.n_refined.item())
+    sparsity = 1.0 - kv_cnt_np.sum() / (BH * Nb * Nb)
+
+    # timed region: per-step events for the attention share
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    time.sleep(0.3)
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_begin.record(stream)
+    for s in range(args.steps):
+        starts[s].record(stream)
+        ev_mid = mids[s]
+        step()
+        ends[s].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    total_ms = t_begin.elapsed_time(t_end)
+    attn_ms = statistics.mean(mids[s].elapsed_time(ends[s]) for s in range(args.steps))
+    mask_ms = statistics.mean(starts[s].elapsed_time(mids[s]) for s in range(args.steps))
+    if ws > 1:
+        t = torch.tensor([total_ms, attn_ms, mask_ms, flop], device=dev, dtype=torch.float64)
+        mx = t.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        total_ms, attn_ms, mask_ms = mx[0].item(), mx[1].item(), mx[2].item()
+        flop_all = sm[3].item()
+    else:
+        flop_all = flop
+    ms_per_step = total_ms / args.steps
+    value = flop_all / (ms_per_step * 1e-3) / 1e12
+
+    # e2e: host buffers through the ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        qp, kp, vp = (t.pin_memory() for t in (q_h, k_h, v_h))
+        o_host = torch.empty_like(q_h).pin_memory()
+        lse_host = torch.empty((BH, N), dtype=torch.float32).pin_memory()
+        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+        def e2e_step():
+            qd.copy_(qp, non_blocking=True)
+            kd.copy_(kp, non_blocking=True)
+            vd.copy_(vp, non_blocking=True)
+            mm = A.blade_asa_mask(qd, kd, unit_offset=unit_offset, want_mask=False, **mp)
+            o, lse = A.blade_bsa_fwd(qd, kd, vd, mm.kv_idx, mm.kv_cnt, impl=impl)
+            o_host.copy_(o, non_blocking=True)
+            lse_host.copy_(lse, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        if ws > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e = {"value": flop_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * q_h.numel() * 2,
+               "d2h_bytes_per_step": q_h.numel() * 2 + BH * N * 4}
+
+    pk, pk_src = peaks()
+    attn_tflops = flop / (attn_ms * 1e-3) / 1e12
+    roof = {"kernel": "blade_bsa_fwd (attention)", "bound": "tensor", "achieved": attn_tflops,
+            "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": attn_tflops / pk["bf16_tflops"],
+            "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)",
+            "traffic": traffic_for(args.workload, "attn"),
+            "attn_ms": attn_ms, "mask_ms": mask_ms,
+            "attn_share": attn_ms / (attn_ms + mask_ms)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        qb = 4 if args.workload != "tiny" else Nb
+        f1, est, desc = oracle_sample(q_h, k_h, v_h, w, mp, qb)
+        cpu = {"value": f1 / est / 1e12, "unit": "TFLOP/s", "cores": cores_used(),
+               "kind": "oracle", "sample": desc}
+
+    launches_per_step = 6 + (1 if mp.get("samples", 16) > 64 else 0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (smooth-field Q/K, iid V; DESIGN.md §Inputs)",
+            "config": {"workload": w.name, "B_total": ws, "H": w.H, "N": N, "d": d,
+                       "mask": mode, "tau": mp["tau"], "keep": [mp["keep_min"], mp["keep_max"]],
+                       "block": 128, "samples": 16, "sparsity": round(float(sparsity), 4),
+                       "parallelism": f"(batch,head)-sharded x{ws}, no collective",
+                       "attn_impl": args.attn, "l2": "inputs larger than L2 (Q+K+V "
+                       f"{3 * q_h.numel() * 2 / 1e6:.0f} MB per rank per step), no flush",
+                       "rows_refined_fp64": refined,
+                       "probe_gflop": probe_flop(BH, N, d) / 1e9},
+            "ms_mask": mask_ms, "ms_attn": attn_ms,
+            "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/*
+ * blade_asa.h — C ABI of the B200-native ASA forward (BLADE, arXiv 2508.10774).
+ *
+ * Two calls make up the hot path of Adaptive Block-Sparse Attention (ASA):
+ *
+ *   blade_asa_mask  Alg. 1 of the paper with Alg. 2/3
+ *                    as the definition of the block importance
+ *                   P_imp: block partition (l.2), random sampling of k tokens
+ *                   per block of Q and K (l.3), the sampled attention
+ *                   softmax(Q_s K_s^T * scale) (l.4), k x k max-pooling to
+ *                   P_imp (l.5), row normalisation, descending sort,
+ *                   cumulative-mass cut at tau and clamping (l.7-9), and the
+ *                   binary mask (l.10), compacted to per-query-block lists of
+ *                   kept key blocks.
+ *   blade_bsa_fwd   block-sparse flash-attention forward ("Standard
+ *                   ASA: the generated binary sparse mask M is directly
+ *                   integrated with a block-sparse attention kernel") over
+ *                   those lists, producing O and the log-sum-exp LSE.
+ *
+ * Conventions shared by every entry point
+ *   - Tensors are caller-owned DEVICE memory, contiguous, layout [BH, N, d]
+ *     with BH = B*H flattened (unit u = b*H + h), so a contiguous range of
+ *     units is a contiguous slice.  Q, K, V, O are bf16 (raw 16-bit words).
+ *   - Nothing is allocated or freed by the library.  Scratch comes from the
+ *     caller's `workspace` (device memory, >= the size the matching
+ *     *_workspace_size() returns, 256-byte aligned).
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream).  Calls never synchronise the host.
+ *   - Arguments are validated synchronously before anything is enqueued; a
+ *     non-OK status means nothing was launched.  Launch failures return
+ *     BLADE_ERR_CUDA (cudaGetLastError).  No C++ exception crosses the ABI.
+ *   - Non-finite inputs give undefined (but memory-safe) outputs.
+ *   - The library is stateless and re-entrant.
+ *   - GPU limits: block (b) == 128; d in {64, 128}; samples (k) in
+ *     {16, 32, 64, 128}; N >= 1; N_b = ceil(N/b) <= 512.  Other values give
+ *     BLADE_ERR_UNSUPPORTED.
+ */
+#ifndef BLADE_ASA_H_
+#define BLADE_ASA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BLADE_OK = 0,
+  BLADE_ERR_INVALID_ARG = 1,   /* NULL / misaligned pointer, bad size or parameter */
+  BLADE_ERR_UNSUPPORTED = 2,   /* valid per the paper but outside the GPU limits above */
+  BLADE_ERR_WORKSPACE = 3,     /* workspace NULL or smaller than *_workspace_size() */
+  BLADE_ERR_CUDA = 4           /* a CUDA launch or runtime call failed */
+} blade_status_t;
+
+/* Mask-generation parameters.  Field readings: DESIGN.md §Readings. */
+typedef struct {
+  int32_t  block;        /* b, query and key block size ("b=128"); GPU: 128       */
+  int32_t  samples;      /* k, tokens sampled per block ("k=16"); 1 <= k <= b     */
+  float    tau;          /* cumulative-mass threshold, 0 < tau <= 1       */
+  int32_t  keep_min;     /* lo: min kept key blocks per query block, >= 1 (P:151 clamp) */
+  int32_t  keep_max;     /* hi: max kept, >= lo; clipped to N_b.  lo == hi: top-k mode  */
+  float    scale;        /* softmax scale, normally (float)(1/sqrt(d))           */
+  uint64_t seed;         /* sampler seed (reading R-1)                                   */
+  int32_t  sample_mode;  /* 0 hash-random (default, R-1), 1 strided, 2 caller-supplied  */
+  int32_t  share_qk;     /* 0: independent Q and K samples; 1: K reuses Q's offsets     */
+  int64_t  unit_offset;  /* global index of this call's first unit (sharding, R-1)      */
+  float    refine_guard; /* relative decision margin below which a row is recomputed in
+                            fp64 (reading R-14); <= 0 selects the default 1e-4          */
+  int32_t  reserved;     /* must be 0                                                    */
+} blade_asa_params_t;
+
+/* Bytes of scratch blade_asa_mask needs for this problem (0 on bad args). */
+size_t blade_asa_mask_workspace_size(int64_t BH, int32_t N, int32_t d,
+                                     const blade_asa_params_t* params);
+
+/*
+ * blade_asa_mask — Alg. 1 l.2-10 for every unit.
+ *   q, k        [BH, N, d] bf16 device, 16-byte aligned (required).
+ *   mask        [BH, N_b, N_b] uint8 0/1 out (optional, may be NULL).
+ *   kv_idx      [BH, N_b, N_b] int32 out (required): row i lists the kept key
+ *               blocks of query block i in ascending order, tail = -1.
+ *   kv_cnt      [BH, N_b] int32 out (required): m of row i, in [lo, hi].
+ *   p_imp       [BH, N_b, N_b] fp32 out (optional): raw max-pooled P_imp of
+ *               Alg. 1 l.5 (before the l.7 normalisation).  Rows decided in
+ *               fp64 (refined) hold that fp64 value rounded to fp32.
+ *   sample_idx  [BH, 2, N_b, k] int32 (optional): in-block offsets of the
+ *               sampled Q ([:,0]) and K ([:,1]) rows, ascending, -1 padded.
+ *               OUTPUT for sample_mode 0/1; INPUT (required) for mode 2.
+ *   n_refined   device int32 scalar out (optional): rows recomputed in fp64.
+ * Errors: INVALID_ARG (NULL q/k/kv_idx/kv_cnt, N < 1, BH < 1, tau out of
+ * (0, 1], lo < 1, hi < lo, k < 1 or k > b, reserved != 0, mode 2 without
+ * sample_idx), UNSUPPORTED (GPU limits), WORKSPACE, CUDA.
+ */
+blade_status_t blade_asa_mask(const void* q, const void* k, int64_t BH, int32_t N,
+                              int32_t d, const blade_asa_params_t* params,
+                              uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
+                              float* p_imp, int32_t* sample_idx, int32_t* n_refined,
+                              void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* Bytes of scratch blade_bsa_fwd needs (0 on bad args). */
+size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block);
+
+/* Attention implementations (the `impl` argument of blade_bsa_fwd). */
+#define BLADE_ATTN_AUTO 0      /* fastest available: tcgen05/TMEM/TMA kernel          */
+#define BLADE_ATTN_TCGEN05 1   /* sm_100a tcgen05 + TMEM + TMA warp-specialised kernel */
+#define BLADE_ATTN_MMA_SYNC 2  /* legacy mma.sync baseline (kept for comparison)       */
+
+/*
+ * blade_bsa_fwd — block-sparse attention over kept blocks.
+ *   For each query row r of query block i and T = union of [j*b, min(j*b+b, N))
+ *   over j in kv_idx[u, i, 0:kv_cnt[u, i]]:
+ *     LSE[r] = ln sum_{t in T} exp(scale * q_r . k_t)            (reading R-10)
+ *     O[r]   = sum_{t in T} exp(scale * q_r . k_t - LSE[r]) * v_t
+ *   q, k, v     [BH, N, d] bf16 device, 16-byte aligned.
+ *   kv_idx      [BH, N_b, N_b] int32, kv_cnt [BH, N_b] int32 (e.g. from
+ *               blade_asa_mask; caller-built lists must hold distinct ids in
+ *               [0, N_b), 1 <= kv_cnt <= N_b; order is free).
+ *   o           [BH, N, d] bf16 out; lse [BH, N] fp32 out (may be NULL).
+ *   impl        BLADE_ATTN_* selector.
+ * Errors: INVALID_ARG, UNSUPPORTED (GPU limits; impl not built), WORKSPACE, CUDA.
+ */
+blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                             int32_t N, int32_t d, int32_t block, float scale,
+                             const int32_t* kv_idx, const int32_t* kv_cnt,
+                             void* o, float* lse, int32_t impl,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* Static, NUL-terminated description of a status code. */
+const char* blade_status_string(blade_status_t status);
+
+/* Library version as 10000*major + 100*minor + patch. */
+int32_t blade_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLADE_ASA_H_ */

@@ -1,0 +1,222 @@
+"""Thin Python binding of the C ABI in include/blade_asa.h.
+
+Argument marshalling only: every step of the ASA forward runs in the CUDA
+kernels of ``lib/libblade_asa.so``.  torch supplies device memory and the
+current stream.  Importing this module fails loudly if the library is
+missing; there is no CPU or PyTorch fallback.
+
+Python names match the ABI:  ``blade_asa_mask``, ``blade_bsa_fwd``.
+``asa_forward`` chains the two (the whole hot path).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libblade_asa.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"{_LIB_PATH} is missing: build it with `python -m paper_2508_10774_b200.build` "
+        "(there is no fallback path)")
+_lib = ctypes.CDLL(_LIB_PATH)
+
+BLADE_OK, BLADE_ERR_INVALID_ARG, BLADE_ERR_UNSUPPORTED, BLADE_ERR_WORKSPACE, BLADE_ERR_CUDA = range(5)
+ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC = 0, 1, 2
+
+ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd_workspace_size",
+               "blade_bsa_fwd", "blade_status_string", "blade_version")
+
+
+class BladeAsaParams(ctypes.Structure):
+    """Mirror of blade_asa_params_t (field order and types must match)."""
+
+    _fields_ = [("block", ctypes.c_int32), ("samples", ctypes.c_int32), ("tau", ctypes.c_float),
+                ("keep_min", ctypes.c_int32), ("keep_max", ctypes.c_int32),
+                ("scale", ctypes.c_float), ("seed", ctypes.c_uint64),
+                ("sample_mode", ctypes.c_int32), ("share_qk", ctypes.c_int32),
+                ("unit_offset", ctypes.c_int64), ("refine_guard", ctypes.c_float),
+                ("reserved", ctypes.c_int32)]
+
+
+_vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+_lib.blade_asa_mask_workspace_size.restype = _sz
+_lib.blade_asa_mask_workspace_size.argtypes = [_i64, _i32, _i32, ctypes.POINTER(BladeAsaParams)]
+_lib.blade_asa_mask.restype = ctypes.c_int
+_lib.blade_asa_mask.argtypes = [_vp, _vp, _i64, _i32, _i32, ctypes.POINTER(BladeAsaParams),
+                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+_lib.blade_bsa_fwd_workspace_size.restype = _sz
+_lib.blade_bsa_fwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
+_lib.blade_bsa_fwd.restype = ctypes.c_int
+_lib.blade_bsa_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp, _vp,
+                               _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_status_string.restype = ctypes.c_char_p
+_lib.blade_status_string.argtypes = [ctypes.c_int]
+_lib.blade_version.restype = _i32
+
+
+class BladeError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {_lib.blade_status_string(status).decode()} (status {status})")
+        self.status = status
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def version() -> int:
+    return int(_lib.blade_version())
+
+
+def default_scale(d: int) -> float:
+    """fp32(1/sqrt(d)) (reading R-3)."""
+    return float(torch.tensor(1.0 / math.sqrt(d), dtype=torch.float32))
+
+
+def num_blocks(N: int, block: int = 128) -> int:
+    return (N + block - 1) // block
+
+
+def keep_count(ratio_ppm: int, Nb: int) -> int:
+    """Fraction (parts per million) of N_b -> block count, integer ceil (>= 1)."""
+    return max(1, (ratio_ppm * Nb + 999_999) // 1_000_000)
+
+
+_workspaces: dict = {}
+
+
+def _workspace(nbytes: int, device: torch.device, tag: str) -> torch.Tensor:
+    key = (device, tag)
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
+        _workspaces[key] = buf
+    off = (-buf.data_ptr()) % 256
+    return buf[off:off + max(nbytes, 256)]
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _as_units(x: torch.Tensor, name: str) -> torch.Tensor:
+    if x.dim() == 4:
+        x = x.reshape(-1, x.shape[2], x.shape[3])
+    if x.dim() != 3 or x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous CUDA bf16 [B,H,N,d] or [BH,N,d] tensor")
+    return x
+
+
+@dataclass
+class MaskOut:
+    kv_idx: torch.Tensor            # [BH, N_b, N_b] int32
+    kv_cnt: torch.Tensor            # [BH, N_b] int32
+    mask: torch.Tensor | None       # [BH, N_b, N_b] uint8
+    p_imp: torch.Tensor | None      # [BH, N_b, N_b] fp32
+    sample_idx: torch.Tensor | None # [BH, 2, N_b, k] int32
+    n_refined: torch.Tensor         # [1] int32 (device)
+
+
+def make_params(*, d: int, tau: float = 0.9, keep_min: int = 1, keep_max: int = 1 << 30,
+                block: int = 128, samples: int = 16, scale: float | None = None, seed: int = 42,
+                sample_mode: int = 0, share_qk: bool = False, unit_offset: int = 0,
+                refine_guard: float = 0.0) -> BladeAsaParams:
+    return BladeAsaParams(block, samples, tau, keep_min, keep_max,
+                          default_scale(d) if scale is None else scale, seed & ((1 << 64) - 1),
+                          sample_mode, int(bool(share_qk)), unit_offset, refine_guard, 0)
+
+
+def blade_asa_mask(q: torch.Tensor, k: torch.Tensor, *, tau: float = 0.9, keep_min: int = 1,
+                   keep_max: int = 1 << 30, block: int = 128, samples: int = 16,
+                   scale: float | None = None, seed: int = 42, sample_mode: int = 0,
+                   share_qk: bool = False, unit_offset: int = 0, refine_guard: float = 0.0,
+                   want_mask: bool = True, want_pimp: bool = False, want_samples: bool = False,
+                   sample_idx: torch.Tensor | None = None, out: MaskOut | None = None,
+                   stream=None) -> MaskOut:
+    """Alg. 1 on the GPU; see blade_asa.h for every argument."""
+    q = _as_units(q, "q")
+    k = _as_units(k, "k")
+    BH, N, d = q.shape
+    if k.shape != q.shape:
+        raise ValueError("q and k shapes differ")
+    prm = make_params(d=d, tau=tau, keep_min=keep_min, keep_max=keep_max, block=block,
+                      samples=samples, scale=scale, seed=seed, sample_mode=sample_mode,
+                      share_qk=share_qk, unit_offset=unit_offset, refine_guard=refine_guard)
+    Nb = num_blocks(N, block)
+    dev = q.device
+    if out is None:
+        if sample_mode == 2 and sample_idx is None:
+            raise ValueError("sample_mode 2 needs sample_idx")
+        out = MaskOut(
+            kv_idx=torch.empty((BH, Nb, Nb), dtype=torch.int32, device=dev),
+            kv_cnt=torch.empty((BH, Nb), dtype=torch.int32, device=dev),
+            mask=torch.empty((BH, Nb, Nb), dtype=torch.uint8, device=dev) if want_mask else None,
+            p_imp=torch.empty((BH, Nb, Nb), dtype=torch.float32, device=dev) if want_pimp else None,
+            sample_idx=(sample_idx if sample_idx is not None else
+                        torch.empty((BH, 2, Nb, samples), dtype=torch.int32, device=dev)
+                        if want_samples else None),
+            n_refined=torch.zeros(1, dtype=torch.int32, device=dev))
+    nbytes = _lib.blade_asa_mask_workspace_size(BH, N, d, ctypes.byref(prm))
+    if nbytes == 0:
+        st = _lib.blade_asa_mask(None, None, BH, N, d, ctypes.byref(prm), None, None, None, None,
+                                 None, None, None, 0, None)
+        raise BladeError(st if st else BLADE_ERR_INVALID_ARG, "blade_asa_mask_workspace_size")
+    ws = _workspace(nbytes, dev, "mask")
+    st = _lib.blade_asa_mask(_ptr(q), _ptr(k), BH, N, d, ctypes.byref(prm), _ptr(out.mask),
+                             _ptr(out.kv_idx), _ptr(out.kv_cnt), _ptr(out.p_imp),
+                             _ptr(out.sample_idx), _ptr(out.n_refined), _ptr(ws), ws.numel(),
+                             _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_asa_mask")
+    return out
+
+
+def blade_bsa_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_idx: torch.Tensor,
+                  kv_cnt: torch.Tensor, *, scale: float | None = None, block: int = 128,
+                  impl: int = ATTN_AUTO, want_lse: bool = True, o: torch.Tensor | None = None,
+                  lse: torch.Tensor | None = None, stream=None):
+    """Block-sparse attention forward over kept blocks -> (O, LSE)."""
+    q = _as_units(q, "q")
+    k = _as_units(k, "k")
+    v = _as_units(v, "v")
+    BH, N, d = q.shape
+    Nb = num_blocks(N, block)
+    for t, nm, shp in ((kv_idx, "kv_idx", (BH, Nb, Nb)), (kv_cnt, "kv_cnt", (BH, Nb))):
+        if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous() or tuple(t.shape) != shp:
+            raise ValueError(f"{nm} must be contiguous CUDA int32 of shape {shp}")
+    if o is None:
+        o = torch.empty_like(q)
+    if lse is None and want_lse:
+        lse = torch.empty((BH, N), dtype=torch.float32, device=q.device)
+    nbytes = _lib.blade_bsa_fwd_workspace_size(BH, N, d, block)
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_fwd_workspace_size")
+    ws = _workspace(nbytes, q.device, "attn")
+    st = _lib.blade_bsa_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, block,
+                            default_scale(d) if scale is None else scale, _ptr(kv_idx),
+                            _ptr(kv_cnt), _ptr(o), _ptr(lse), impl, _ptr(ws), ws.numel(),
+                            _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_bsa_fwd")
+    return o, lse
+
+
+def asa_forward(q, k, v, *, tau: float = 0.9, keep_min: int = 1, keep_max: int = 1 << 30,
+                samples: int = 16, seed: int = 42, unit_offset: int = 0,
+                impl: int = ATTN_AUTO, stream=None, **mask_kw):
+    """The whole ASA forward: mask generation then block-sparse attention.
+    Returns (O, LSE, MaskOut)."""
+    m = blade_asa_mask(q, k, tau=tau, keep_min=keep_min, keep_max=keep_max, samples=samples,
+                       seed=seed, unit_offset=unit_offset, stream=stream, **mask_kw)
+    o, lse = blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl, stream=stream)
+    return o, lse, m

@@ -1,0 +1,138 @@
+// abi.cu — the extern "C" boundary declared in include/blade_asa.h:
+// synchronous validation, workspace accounting, and dispatch to the kernel
+// launchers.  No allocation, no host synchronisation, no exceptions.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/blade_asa.h"
+#include "internal.h"
+
+namespace {
+
+using blade::AttnProblem;
+using blade::MaskProblem;
+
+constexpr int kGpuBlock = 128;
+constexpr int kMaxNb = 512;
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+blade_status_t make_mask_problem(int64_t BH, int32_t N, int32_t d,
+                                 const blade_asa_params_t* prm, MaskProblem* out) {
+  if (!prm || BH < 1 || N < 1 || d < 1) return BLADE_ERR_INVALID_ARG;
+  if (prm->block < 1 || prm->samples < 1 || prm->samples > prm->block) return BLADE_ERR_INVALID_ARG;
+  if (!(prm->tau > 0.f && prm->tau <= 1.f)) return BLADE_ERR_INVALID_ARG;
+  if (prm->keep_min < 1 || prm->keep_max < prm->keep_min) return BLADE_ERR_INVALID_ARG;
+  if (prm->sample_mode < 0 || prm->sample_mode > 2 || prm->reserved != 0) return BLADE_ERR_INVALID_ARG;
+  if (!(prm->scale > 0.f) || !isfinite(prm->scale)) return BLADE_ERR_INVALID_ARG;
+  if (prm->unit_offset < 0) return BLADE_ERR_INVALID_ARG;
+  if (prm->block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  if (prm->samples != 16 && prm->samples != 32 && prm->samples != 64 && prm->samples != 128)
+    return BLADE_ERR_UNSUPPORTED;
+  const int64_t Nb = (int64_t(N) + prm->block - 1) / prm->block;
+  if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
+  MaskProblem p{};
+  p.BH = BH;
+  p.N = N;
+  p.d = d;
+  p.b = prm->block;
+  p.kk = prm->samples;
+  p.Nb = int(Nb);
+  p.tau = double(prm->tau);  // the fp32 value, widened exactly (reading R-5)
+  p.lo = int(prm->keep_min < Nb ? prm->keep_min : Nb);
+  p.hi = int(prm->keep_max < Nb ? prm->keep_max : Nb);
+  if (p.hi < p.lo) p.hi = p.lo;
+  p.scale = prm->scale;
+  p.seed = prm->seed;
+  p.mode = prm->sample_mode;
+  p.share_qk = prm->share_qk ? 1 : 0;
+  p.unit_offset = prm->unit_offset;
+  p.guard = prm->refine_guard > 0.f ? double(prm->refine_guard) : 1e-4;
+  *out = p;
+  return BLADE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t blade_asa_mask_workspace_size(int64_t BH, int32_t N, int32_t d,
+                                     const blade_asa_params_t* params) {
+  MaskProblem p;
+  if (make_mask_problem(BH, N, d, params, &p) != BLADE_OK) return 0;
+  return blade::mask_workspace_layout(p).total;
+}
+
+blade_status_t blade_asa_mask(const void* q, const void* k, int64_t BH, int32_t N, int32_t d,
+                              const blade_asa_params_t* params, uint8_t* mask,
+                              int32_t* kv_idx, int32_t* kv_cnt, float* p_imp,
+                              int32_t* sample_idx, int32_t* n_refined, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (!q || !k || !kv_idx || !kv_cnt) return BLADE_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(k)) return BLADE_ERR_INVALID_ARG;
+  MaskProblem p;
+  blade_status_t st = make_mask_problem(BH, N, d, params, &p);
+  if (st != BLADE_OK) return st;
+  if (p.mode == 2 && !sample_idx) return BLADE_ERR_INVALID_ARG;
+  const size_t need = blade::mask_workspace_layout(p).total;
+  if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return BLADE_ERR_WORKSPACE;
+  cudaError_t e = blade::launch_mask(p, q, k, mask, kv_idx, kv_cnt, p_imp, sample_idx, n_refined,
+                                     static_cast<char*>(workspace),
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+
+size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block) {
+  if (BH < 1 || N < 1 || block != kGpuBlock || (d != 64 && d != 128)) return 0;
+  AttnProblem p{BH, N, d, block, int((N + block - 1) / block), 1.f};
+  size_t a = blade::attn_tc_workspace(p);
+  return a < 256 ? 256 : a;
+}
+
+blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                             int32_t N, int32_t d, int32_t block, float scale,
+                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
+                             int32_t impl, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  if (!q || !k || !v || !kv_idx || !kv_cnt || !o) return BLADE_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
+  if (BH < 1 || N < 1 || block < 1 || !(scale > 0.f) || !isfinite(scale)) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_MMA_SYNC) return BLADE_ERR_INVALID_ARG;
+  if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  const int64_t Nb = (int64_t(N) + block - 1) / block;
+  if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
+  AttnProblem p{BH, N, d, block, int(Nb), scale};
+  const size_t need = blade_bsa_fwd_workspace_size(BH, N, d, block);
+  if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return BLADE_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (impl == BLADE_ATTN_MMA_SYNC) {
+    e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
+  } else {
+    e = blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
+                              static_cast<char*>(workspace), workspace_bytes, s);
+    if (e == cudaErrorNotSupported) {
+      if (impl == BLADE_ATTN_TCGEN05) return BLADE_ERR_UNSUPPORTED;
+      e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
+    }
+  }
+  return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+
+const char* blade_status_string(blade_status_t status) {
+  switch (status) {
+    case BLADE_OK: return "ok";
+    case BLADE_ERR_INVALID_ARG: return "invalid argument";
+    case BLADE_ERR_UNSUPPORTED: return "unsupported on this GPU path (see blade_asa.h limits)";
+    case BLADE_ERR_WORKSPACE: return "workspace missing, misaligned or too small";
+    case BLADE_ERR_CUDA: return "CUDA launch/runtime error";
+  }
+  return "unknown status";
+}
+
+int32_t blade_version(void) { return 100; }
+
+}  // extern "C"

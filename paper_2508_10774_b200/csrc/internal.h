@@ -1,0 +1,72 @@
+// internal.h — launcher declarations and workspace layout shared by the
+// C-ABI front end (abi.cu) and the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace blade {
+
+struct MaskProblem {
+  int64_t BH;
+  int N, d, b, kk, Nb;
+  double tau;
+  int lo, hi;
+  float scale;
+  uint64_t seed;
+  int mode, share_qk;
+  int64_t unit_offset;
+  double guard;
+};
+
+// Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
+struct MaskWorkspace {
+  size_t off_qs, off_ks, off_pimp, off_counters, off_flags, off_r64, off_mpart,
+      off_lpart, total;
+  int nchunks;  // refine key chunks of 256 sampled keys
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
+  MaskWorkspace w{};
+  const size_t rows = size_t(p.BH) * p.Nb;            // (unit, q-block) rows
+  const size_t nk = size_t(p.Nb) * p.kk;              // padded sampled rows / unit
+  w.nchunks = int((nk + 255) / 256);
+  size_t o = 0;
+  w.off_qs = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);
+  w.off_ks = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);
+  w.off_pimp = o;     o = align256(o + rows * p.Nb * 4);
+  w.off_counters = o; o = align256(o + 64);
+  w.off_flags = o;    o = align256(o + rows * 4);
+  w.off_r64 = o;      o = align256(o + rows * p.kk * p.Nb * 8);
+  w.off_mpart = o;    o = align256(o + rows * w.nchunks * p.kk * 8);
+  w.off_lpart = o;    o = align256(o + rows * w.nchunks * p.kk * 8);
+  w.total = o;
+  return w;
+}
+
+cudaError_t launch_mask(const MaskProblem& p, const void* q, const void* k, uint8_t* mask,
+                        int32_t* kv_idx, int32_t* kv_cnt, float* p_imp_out,
+                        int32_t* sample_idx, int32_t* n_refined, char* ws,
+                        cudaStream_t stream);
+
+struct AttnProblem {
+  int64_t BH;
+  int N, d, b, Nb;
+  float scale;
+};
+
+cudaError_t launch_attn_mma(const AttnProblem& p, const void* q, const void* k,
+                            const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
+                            void* o, float* lse, cudaStream_t stream);
+
+// Returns cudaErrorNotSupported when the tcgen05 path is not available.
+cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k,
+                           const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
+                           void* o, float* lse, char* ws, size_t ws_bytes,
+                           cudaStream_t stream);
+size_t attn_tc_workspace(const AttnProblem& p);
+
+}  // namespace blade

@@ -1,0 +1,112 @@
+"""Host-side checks of the C-ABI library (no GPU needed, no compute calls):
+the library loads, exports every function include/blade_asa.h declares,
+and its synchronous validation returns the documented status codes."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "blade_asa.h")
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(blade_[a-z_0-9]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def asa():
+    from paper_2508_10774_b200 import asa as A
+    return A
+
+
+def test_header_declares_the_boundary():
+    fns = _declared_functions()
+    assert {"blade_asa_mask", "blade_bsa_fwd"} <= set(fns)
+
+
+def test_library_exports_every_declared_symbol(asa):
+    lib = ctypes.CDLL(asa.library_path())
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+    assert set(asa.ABI_SYMBOLS) == set(_declared_functions())
+
+
+def test_params_struct_layout(asa):
+    # blade_asa_params_t: 4+4+4+4+4+4 (+0 pad) +8 +4+4 +8 +4+4 = 56 bytes
+    assert ctypes.sizeof(asa.BladeAsaParams) == 56
+    assert asa.BladeAsaParams.seed.offset == 24
+    assert asa.BladeAsaParams.unit_offset.offset == 40
+
+
+def test_status_strings_and_version(asa):
+    lib = asa._lib
+    for s in range(5):
+        assert lib.blade_status_string(s)
+    assert asa.version() >= 100
+
+
+def test_workspace_sizes(asa):
+    lib = asa._lib
+    p = asa.make_params(d=128, tau=0.9)
+    w1 = lib.blade_asa_mask_workspace_size(12, 32760, 128, ctypes.byref(p))
+    # Q_s + K_s + fp32 P_imp + fp64 refine stash for every row
+    assert w1 >= 2 * 12 * 256 * 16 * 128 * 2 + 12 * 256 * 256 * 4 + 12 * 256 * 16 * 256 * 8
+    assert lib.blade_asa_mask_workspace_size(12, 32760, 96, ctypes.byref(p)) == 0  # d unsupported
+    assert lib.blade_bsa_fwd_workspace_size(12, 32760, 128, 128) >= 256
+    assert lib.blade_bsa_fwd_workspace_size(12, 32760, 128, 64) == 0
+
+
+def _mask_call(asa, q=1 << 20, k=1 << 20, BH=1, N=512, d=64, prm=None, kv_idx=1 << 20,
+               kv_cnt=1 << 20, ws=1 << 20, wsb=1 << 40, sample_idx=None):
+    prm = prm or asa.make_params(d=d)
+    return asa._lib.blade_asa_mask(q, k, BH, N, d, ctypes.byref(prm), None, kv_idx, kv_cnt, None,
+                                   sample_idx, None, ws, wsb, None)
+
+
+def test_mask_validation_codes(asa):
+    A = asa
+    assert _mask_call(A, q=None) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, q=(1 << 20) + 2) == A.BLADE_ERR_INVALID_ARG          # misaligned
+    assert _mask_call(A, kv_cnt=None) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, N=0) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, tau=0.0)) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, tau=1.5)) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, keep_min=0)) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, keep_min=5, keep_max=4)) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, samples=200)) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, sample_mode=2)) == A.BLADE_ERR_INVALID_ARG
+    assert _mask_call(A, prm=A.make_params(d=64, block=64)) == A.BLADE_ERR_UNSUPPORTED
+    assert _mask_call(A, prm=A.make_params(d=64, samples=8)) == A.BLADE_ERR_UNSUPPORTED
+    assert _mask_call(A, d=80, prm=A.make_params(d=80)) == A.BLADE_ERR_UNSUPPORTED
+    assert _mask_call(A, N=128 * 600) == A.BLADE_ERR_UNSUPPORTED               # N_b > 512
+    assert _mask_call(A, ws=None) == A.BLADE_ERR_WORKSPACE
+    assert _mask_call(A, wsb=16) == A.BLADE_ERR_WORKSPACE
+    assert _mask_call(A, ws=(1 << 20) + 16) == A.BLADE_ERR_WORKSPACE
+
+
+def test_attn_validation_codes(asa):
+    A, lib = asa, asa._lib
+    P = 1 << 20
+
+    def call(q=P, o=P, BH=1, N=512, d=64, block=128, scale=0.125, impl=0, ws=P, wsb=1 << 40):
+        return lib.blade_bsa_fwd(q, P, P, BH, N, d, block, scale, P, P, o, None, impl, ws, wsb,
+                                 None)
+
+    assert call(q=None) == A.BLADE_ERR_INVALID_ARG
+    assert call(o=P + 8) == A.BLADE_ERR_INVALID_ARG
+    assert call(scale=0.0) == A.BLADE_ERR_INVALID_ARG
+    assert call(impl=7) == A.BLADE_ERR_INVALID_ARG
+    assert call(block=64) == A.BLADE_ERR_UNSUPPORTED
+    assert call(d=256) == A.BLADE_ERR_UNSUPPORTED
+    assert call(ws=None) == A.BLADE_ERR_WORKSPACE
+
+
+def test_keep_count_integer_rounding(asa):
+    assert asa.keep_count(50_000, 256) == 13          # ceil(0.05 * 256)
+    assert asa.keep_count(200_000, 256) == 52
+    assert asa.keep_count(1, 4) == 1

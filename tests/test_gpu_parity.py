@@ -1,0 +1,154 @@
+"""CUDA path vs the fp64 oracle, element by element, through the C ABI.
+
+Masks: bit-exact (kv_idx, kv_cnt, mask; sample offsets always bit-exact)
+outside the 1e-6 tie band; attention (given the oracle's mask, so mask ties
+cannot leak in): O max abs <= 2e-2, mean abs <= 2e-3, LSE abs <= 1e-3."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import asa_oracle as O
+from paper_2508_10774_b200 import inputs
+
+from . import _parity as PT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A(cuda_dev):
+    from paper_2508_10774_b200 import asa
+    return asa
+
+
+IMPLS = [pytest.param(2, id="mma_sync"), pytest.param(1, id="tcgen05")]
+
+
+def _run_mask(A, q, k, p: O.AsaParams, **kw):
+    return A.blade_asa_mask(q.cuda(), k.cuda(), tau=p.tau, keep_min=p.keep_min,
+                            keep_max=p.keep_max, block=p.block, samples=p.samples,
+                            seed=p.seed, sample_mode=p.sample_mode, share_qk=p.share_qk,
+                            unit_offset=p.unit_offset, want_pimp=True, want_samples=True, **kw)
+
+
+MASK_CASES = [
+    # (B, H, N, d, recipe, params)
+    (1, 1, 512, 64, "iid", dict(tau=0.9, keep_min=1, keep_max=4)),       # BJ configs[0]
+    (1, 1, 512, 64, "smooth", dict(tau=0.9)),
+    (1, 2, 512, 128, "smooth", dict(tau=0.95)),
+    (1, 2, 300, 64, "iid", dict(tau=0.8)),                                # ragged tail, k_i = 16
+    (1, 1, 70, 64, "iid", dict(tau=0.5)),                                 # N < b
+    (1, 1, 1000, 128, "smooth", dict(tau=0.9, keep_min=2, keep_max=5)),
+    (1, 1, 129, 64, "iid", dict(tau=0.9)),                                # last block 1 row
+    (1, 3, 2000, 64, "smooth", dict(tau=0.9, samples=32)),
+    (1, 2, 1500, 128, "iid", dict(tau=0.7, samples=64)),
+    (1, 1, 700, 64, "smooth", dict(tau=0.9, samples=128)),                # k = b exhaustive
+    (1, 2, 777, 64, "smooth", dict(tau=1.0)),                             # dense
+    (1, 2, 640, 64, "smooth", dict(tau=0.9, keep_min=3, keep_max=3)),     # top-k mode
+    (1, 2, 640, 64, "smooth", dict(tau=0.9, share_qk=True)),
+    (1, 2, 640, 64, "smooth", dict(tau=0.9, sample_mode=1)),              # strided
+    (1, 2, 640, 64, "smooth", dict(tau=0.9, unit_offset=7, seed=123)),
+    (2, 3, 4096, 128, "smooth", dict(tau=0.9)),
+]
+
+
+def _inputs(B, H, N, d, recipe, seed=42):
+    if recipe == "iid":
+        return inputs.iid(B, H, N, d, seed)
+    return inputs.smooth(B, H, N, d, (1, 1, N), ell=3.0, beta=9.0, seed=seed)
+
+
+@pytest.mark.parametrize("case", MASK_CASES, ids=lambda c: f"{c[0]}x{c[1]}x{c[2]}x{c[3]}-{c[4]}-{c[5]}")
+def test_mask_parity(A, case):
+    B, H, N, d, recipe, kw = case
+    q, k, _ = _inputs(B, H, N, d, recipe)
+    p = O.AsaParams(**kw)
+    ref = O.asa_mask(q, k, p)
+    got = _run_mask(A, q, k, p)
+    torch.cuda.synchronize()
+    assert (got.sample_idx.cpu().numpy() == ref.sample_idx).all()
+    stats = PT.check_mask(ref, got, p)
+    # fp32 probe vs fp64 oracle P_imp (rows decided in fp64 are closer still)
+    np.testing.assert_allclose(got.p_imp.cpu().numpy(), ref.p_imp, rtol=2e-4, atol=1e-9)
+    assert stats["exempt"] <= max(2, stats["rows"] // 20)
+
+
+def test_supplied_samples_mode(A):
+    q, k, _ = _inputs(1, 2, 900, 64, "smooth")
+    p = O.AsaParams(tau=0.85, seed=5)
+    ref = O.asa_mask(q, k, p)
+    sidx = torch.from_numpy(ref.sample_idx).cuda()
+    got = A.blade_asa_mask(q.cuda(), k.cuda(), tau=0.85, sample_mode=2, sample_idx=sidx,
+                           want_pimp=True)
+    torch.cuda.synchronize()
+    PT.check_mask(ref, got, p)
+
+
+@pytest.mark.parametrize("recipe", ["const", "spike"])
+def test_mask_adversarial(A, recipe):
+    if recipe == "const":
+        q, k, _ = inputs.const(2, 600, 64)
+    else:
+        q, k, _ = inputs.spike(2, 600, 64)
+    p = O.AsaParams(tau=0.9)
+    ref = O.asa_mask(q, k, p)
+    got = _run_mask(A, q, k, p)
+    torch.cuda.synchronize()
+    PT.check_mask(ref, got, p)
+
+
+ATTN_CASES = [
+    (1, 1, 512, 64, 0.5), (1, 2, 512, 128, 0.3), (1, 2, 300, 64, 0.6), (1, 1, 70, 128, 1.0),
+    (1, 1, 129, 64, 0.7), (2, 2, 1000, 128, 0.4), (1, 3, 2048, 64, 1.0), (1, 1, 4000, 128, 0.1),
+]
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("case", ATTN_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_attention_parity_given_mask(A, case, impl):
+    B, H, N, d, density = case
+    q, k, v = inputs.iid(B, H, N, d, seed=N + d)
+    BH, Nb = B * H, O.num_blocks(N, 128)
+    rng = np.random.default_rng(N)
+    kv_idx = np.full((BH, Nb, Nb), -1, np.int32)
+    kv_cnt = np.zeros((BH, Nb), np.int32)
+    for u in range(BH):
+        for i in range(Nb):
+            keep = np.flatnonzero(rng.random(Nb) < density)
+            if keep.size == 0:
+                keep = np.array([rng.integers(Nb)])
+            kv_idx[u, i, :keep.size] = keep
+            kv_cnt[u, i] = keep.size
+    o_ref, lse_ref = O.sparse_attention(q, k, v, kv_idx, kv_cnt, 128)
+    qd, kd, vd = PT.to_dev(q, k, v)
+    ki, kc = PT.lists_to_dev(kv_idx, kv_cnt)
+    o, lse = A.blade_bsa_fwd(qd, kd, vd, ki, kc, impl=impl)
+    torch.cuda.synchronize()
+    PT.check_attention(o, lse, o_ref, lse_ref)
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_end_to_end_tiny(A, impl):
+    """BASELINE.json configs[0]: tiny, fixed seed, ASA mask + sparse attention."""
+    q, k, v = inputs.make("tiny", "iid")
+    p = O.AsaParams(tau=0.9, keep_min=1, keep_max=4)
+    ref = O.asa_mask(q, k, p)
+    qd, kd, vd = PT.to_dev(q, k, v)
+    o, lse, m = A.asa_forward(qd, kd, vd, tau=0.9, keep_min=1, keep_max=4, impl=impl)
+    torch.cuda.synchronize()
+    PT.check_mask(ref, m, p)
+    o_ref, lse_ref = O.sparse_attention(q, k, v, m.kv_idx.cpu().numpy(), m.kv_cnt.cpu().numpy(), 128)
+    PT.check_attention(o, lse, o_ref, lse_ref)
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_invariants_ones_and_determinism(A, impl):
+    q, k, _ = inputs.smooth(1, 2, 1000, 128, (1, 1, 1000), seed=3)
+    v = torch.ones_like(q)
+    qd, kd, vd = PT.to_dev(q, k, v)
+    o1, l1, m1 = A.asa_forward(qd, kd, vd, tau=0.9, impl=impl)
+    o2, l2, m2 = A.asa_forward(qd, kd, vd, tau=0.9, impl=impl)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2) and torch.equal(m1.kv_idx, m2.kv_idx)
+    assert (o1.float() - 1).abs().max().item() <= 4e-3          # V = 1 => O = 1
