@@ -165,7 +165,7 @@ def blade_asa_mask(q: torch.Tensor, k: torch.Tensor, *, tau: float = 0.9, keep_m
             sample_idx=(sample_idx if sample_idx is not None else
                         torch.empty((BH, 2, Nb, samples), dtype=torch.int32, device=dev)
                         if want_samples else None),
-            n_refined=torch.zeros(1, dtype=torch.int32, device=dev))
+            n_refined=torch.empty(1, dtype=torch.int32, device=dev))
     nbytes = _lib.blade_asa_mask_workspace_size(BH, N, d, ctypes.byref(prm))
     if nbytes == 0:
         st = _lib.blade_asa_mask(None, None, BH, N, d, ctypes.byref(prm), None, None, None, None,
