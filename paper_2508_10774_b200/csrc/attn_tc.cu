@@ -31,6 +31,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
+#include "tma_host.h"
 
 namespace blade {
 namespace {
@@ -368,39 +369,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef TC_DBG
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// [BH, N, d] bf16 viewed as 3-D (d, N, BH); box 64 x 128 x 1, 128-byte swizzle.
-bool make_map(CUtensorMap* m, const void* base, int64_t BH, int N, int D) {
-  auto enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(N), cuuint64_t(BH)};
-  cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(N) * D * 2};
-  cuuint32_t box[3] = {64, 128, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int D>
 cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                      const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
                      cudaStream_t stream) {
   CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, q, p.BH, p.N, D) || !make_map(&mk, k, p.BH, p.N, D) ||
-      !make_map(&mv, v, p.BH, p.N, D))
+  if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mk, k, p.BH, p.N, D) ||
+      !make_tile_map(&mv, v, p.BH, p.N, D))
     return cudaErrorNotSupported;
   constexpr int smem = Cfg<D>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<D>,

@@ -52,6 +52,10 @@ cudaError_t launch_mask(const MaskProblem& p, const void* q, const void* k, uint
                         int32_t* sample_idx, int32_t* n_refined, char* ws,
                         cudaStream_t stream);
 
+bool probe_tc_supported(int d, int kk, int Nb);
+cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
+                            const void* qs, const void* ks, float* pimp, cudaStream_t stream);
+
 struct AttnProblem {
   int64_t BH;
   int N, d, b, Nb;

@@ -498,46 +498,52 @@ __global__ void __launch_bounds__(256) refine_partial_kernel(
 }
 
 // K-mask.4b  combine the partials of each queued row into its fp64 P_imp row
-// (Alg. 3 l.14, l.17-19) and reselect it.
-__global__ void __launch_bounds__(SEL_WARPS * 32) refine_final_kernel(
+// (Alg. 3 l.14, l.17-19) and reselect it.  One CTA per queued row: threads
+// own query rows for the combine, key blocks for the max-pool, then warp 0
+// reruns the selection on the fp64 row.
+constexpr int RF_THREADS = 256;
+
+__global__ void __launch_bounds__(RF_THREADS) refine_final_kernel(
     int Nb, int N, int b, int kk, int nchunks, double tau, int lo, int hi,
     const int* __restrict__ counters, const int32_t* __restrict__ flags,
     const double* __restrict__ r64, const double* __restrict__ mpart,
     const double* __restrict__ lpart, float* __restrict__ pimp, uint8_t* __restrict__ mask,
     int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt, int32_t* n_refined) {
   extern __shared__ __align__(128) char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  SelScratch& sc = reinterpret_cast<SelScratch*>(smem)[warp];
-  double* sMs = reinterpret_cast<double*>(smem + SEL_WARPS * sizeof(SelScratch)) + warp * 256;
+  SelScratch& sc = *reinterpret_cast<SelScratch*>(smem);
+  double* sMs = reinterpret_cast<double*>(smem + sizeof(SelScratch));
   double* sLs = sMs + 128;
+  const int tid = threadIdx.x;
   const int nflag = counters[0];
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n_refined) *n_refined = nflag;
-  for (int f = blockIdx.x * SEL_WARPS + warp; f < nflag; f += gridDim.x * SEL_WARPS) {
+  if (blockIdx.x == 0 && tid == 0 && n_refined) *n_refined = nflag;
+  for (int f = blockIdx.x; f < nflag; f += gridDim.x) {
     const int64_t row = flags[f];
     const int i = int(row % Nb);
     const int ki = min(kk, min(b, N - i * b));
-    for (int s = lane; s < ki; s += 32) {
+    __syncthreads();
+    if (tid < ki) {
       double M = -INFINITY;
-      for (int c = 0; c < nchunks; ++c) M = fmax(M, mpart[(int64_t(f) * nchunks + c) * kk + s]);
+      for (int c = 0; c < nchunks; ++c) M = fmax(M, mpart[(int64_t(f) * nchunks + c) * kk + tid]);
       double l = 0.0;
       for (int c = 0; c < nchunks; ++c) {
-        const int64_t o = (int64_t(f) * nchunks + c) * kk + s;
+        const int64_t o = (int64_t(f) * nchunks + c) * kk + tid;
         if (mpart[o] != -INFINITY) l += lpart[o] * exp(mpart[o] - M);
       }
-      sMs[s] = M;
-      sLs[s] = l;
+      sMs[tid] = M;
+      sLs[tid] = l;
     }
-    __syncwarp();
-    for (int j = lane; j < Nb; j += 32) {
+    __syncthreads();
+    for (int j = tid; j < Nb; j += RF_THREADS) {
       double best = 0.0;
       for (int s = 0; s < ki; ++s)
         best = fmax(best, exp(r64[(int64_t(f) * kk + s) * Nb + j] - sMs[s]) / sLs[s]);
       sc.val[j] = best;
       if (pimp) pimp[row * Nb + j] = float(best);
     }
-    __syncwarp();
-    select_row_warp(sc, Nb, tau, lo, hi, 0.0, false, mask ? mask + row * Nb : nullptr,
-                    kv_idx + row * Nb, kv_cnt + row);
+    __syncthreads();
+    if (tid < 32)
+      select_row_warp(sc, Nb, tau, lo, hi, 0.0, false, mask ? mask + row * Nb : nullptr,
+                      kv_idx + row * Nb, kv_cnt + row);
   }
 }
 
@@ -564,11 +570,15 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
         ks, counters);
   }
+  if (probe_tc_supported(D, p.kk, p.Nb)) {  // K-mask.2 on tcgen05 (k in {16, 32}, N_b <= 256)
+    cudaError_t e = launch_probe_tc(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
+    if (e != cudaSuccess) return e;
+  } else {
   if (p.kk > PR_ROWS) {
     cudaError_t e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);
     if (e != cudaSuccess) return e;
   }
-  {  // K-mask.2
+  {  // K-mask.2 (mma.sync fallback for other k / longer sequences)
     const size_t smem = size_t(PR_ROWS) * D * 2 + 2 * PR_KEYS * D * 2 +
                         size_t(PR_ROWS) * p.Nb * 4 + 2 * PR_ROWS * 4;
     cudaError_t e = cudaFuncSetAttribute(probe_kernel<D>,
@@ -577,6 +587,7 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     dim3 grid(unsigned((p.Nb * p.kk + PR_ROWS - 1) / PR_ROWS), unsigned(p.BH));
     probe_kernel<D><<<grid, 128, smem, stream>>>(qs, ks, p.N, p.Nb, p.b, p.kk,
                                                  p.scale * kLog2e, pimp);
+  }
   }
   const size_t sel_smem = SEL_WARPS * sizeof(SelScratch);
   {  // K-mask.3
@@ -592,12 +603,8 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     refine_partial_kernel<D><<<148 * 4, 256, 0, stream>>>(
         qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, counters, flags, r64, mpart,
         lpart);
-    const size_t fsmem = sel_smem + SEL_WARPS * 256 * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(refine_final_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(fsmem));
-    if (e != cudaSuccess) return e;
-    refine_final_kernel<<<148, SEL_WARPS * 32, fsmem, stream>>>(
+    const size_t fsmem = sizeof(SelScratch) + 256 * sizeof(double);
+    refine_final_kernel<<<148, RF_THREADS, fsmem, stream>>>(
         p.Nb, p.N, p.b, p.kk, w.nchunks, p.tau, p.lo, p.hi, counters, flags, r64, mpart, lpart,
         p_imp_out, mask, kv_idx, kv_cnt, n_refined);
   }

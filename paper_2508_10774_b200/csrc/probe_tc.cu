@@ -1,0 +1,255 @@
+// probe_tc.cu — K-mask.2 on the 5th-gen tensor cores: the sampled attention
+// prober of PAPER.md Alg. 1 l.4-5 in the streaming form of Alg. 3
+// (GetMaxPooledAttnMap).
+//
+// CTA = 128 sampled query rows (M = 128) of one unit, streaming every
+// 128-key tile of that unit's sampled keys K_s:
+//   warps 0-3  row statistics, thread = sampled query row = TMEM lane:
+//              running max M and sum l of e^{s - M} over all sampled keys
+//              (l.12-15), and the per-(row, key-block) max R (l.15) kept in
+//              TMEM beside the S buffers; at the end
+//              P_imp[i, j] = max over the k rows of block i of e^{R - M} / l
+//              (l.17-19) with a 16/32-lane shuffle max.
+//   warp  4    tcgen05.mma issuer (S = Q_s K_s^T, double-buffered in TMEM)
+//   warp  5    TMA producer (Q_s tile once, K_s tiles through a smem ring)
+// TMEM: S0 [0,128) S1 [128,256) R [256, 256 + N_b)  (N_b <= 256).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tc_ptx.cuh"
+#include "tma_host.h"
+
+namespace blade {
+namespace {
+
+template <int D>
+struct PCfg {
+  static constexpr int kTile = 128 * D * 2;
+  static constexpr int kPanels = D / 64;
+  static constexpr int kPanel = 128 * 128;
+  static constexpr int kRing = D == 128 ? 4 : 8;
+  static constexpr int kOffRing = kTile;
+  static constexpr int kOffBar = kOffRing + kRing * kTile;
+  static constexpr int kNumBar = 1 + 2 * kRing + 4;
+  static constexpr int kOffMisc = kOffBar + kNumBar * 8;
+  static constexpr int kSmem = kOffMisc + 16 + 1024;
+};
+
+constexpr int kPThreads = 256;
+
+template <int D, int KK>
+__global__ void __launch_bounds__(kPThreads, 1)
+    probe_tc_kernel(const __grid_constant__ CUtensorMap tmQs, const __grid_constant__ CUtensorMap tmKs,
+                    int N, int Nb, int b, float scale_log2, float* __restrict__ pimp) {
+  using C = PCfg<D>;
+  constexpr int G = 128 / KK;  // key blocks per 128-key tile
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  char* sQ = smem;
+  char* sRing = smem + C::kOffRing;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* bar_q = bars;
+  uint64_t* bar_full = bars + 1;
+  uint64_t* bar_empty = bars + 1 + C::kRing;
+  uint64_t* bar_s = bars + 1 + 2 * C::kRing;   // [2] S buffer written
+  uint64_t* bar_f = bar_s + 2;                  // [2] S buffer read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t u = blockIdx.y;
+  const int row0 = blockIdx.x * 128;
+  const int NK = Nb * KK;
+  const int ntiles = (NK + 127) / 128;
+  const int k_last = min(KK, N - (Nb - 1) * b);
+  const int first_invalid = (Nb - 1) * KK + k_last;  // sampled columns >= this are padding
+
+  if (warp == 5 && lane == 0) {
+    tc::mbar_init(bar_q, 1);
+    for (int s = 0; s < C::kRing; ++s) {
+      tc::mbar_init(bar_full + s, 1);
+      tc::mbar_init(bar_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      tc::mbar_init(bar_s + t, 1);
+      tc::mbar_init(bar_f + t, 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 4) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 5) {
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&tmQs);
+      tc::tma_prefetch_desc(&tmKs);
+      tc::mbar_arrive_expect_tx(bar_q, C::kTile);
+      for (int p = 0; p < C::kPanels; ++p)
+        tc::tma_load_3d(sQ + p * C::kPanel, &tmQs, bar_q, p * 64, row0, int(u));
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t % C::kRing;
+        tc::mbar_wait(bar_empty + s, ((t / C::kRing) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(bar_full + s, C::kTile);
+        for (int p = 0; p < C::kPanels; ++p)
+          tc::tma_load_3d(sRing + s * C::kTile + p * C::kPanel, &tmKs, bar_full + s, p * 64,
+                          t * 128, int(u));
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
+      const uint32_t qa = smem_u32(sQ), rb = smem_u32(sRing);
+      tc::mbar_wait(bar_q, 0);
+      tc::fence_after_sync();
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t % C::kRing, bsel = t & 1;
+        tc::mbar_wait(bar_full + s, (t / C::kRing) & 1);
+        if (t >= 2) tc::mbar_wait(bar_f + bsel, ((t >> 1) - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t kb = rb + s * C::kTile;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
+          tc::mma_ss(tmem + bsel * 128, tc::sw128_desc(qa + off, 16, 1024),
+                     tc::sw128_desc(kb + off, 16, 1024), idS, ks > 0);
+        }
+        tc::commit(bar_s + bsel);
+        tc::commit(bar_empty + s);
+      }
+    }
+  } else if (warp < 4) {
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < ntiles; ++t) {
+      const int bsel = t & 1;
+      tc::mbar_wait(bar_s + bsel, (t >> 1) & 1);
+      tc::fence_after_sync();
+      float s[128];
+      {
+        uint32_t r0[32], r1[32], r2[32], r3[32];
+        const uint32_t ta = tmem + lane_base + bsel * 128;
+        tc::ld_32x32b_x32(ta + 0, r0);
+        tc::ld_32x32b_x32(ta + 32, r1);
+        tc::ld_32x32b_x32(ta + 64, r2);
+        tc::ld_32x32b_x32(ta + 96, r3);
+        tc::wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          s[e] = __uint_as_float(r0[e]);
+          s[32 + e] = __uint_as_float(r1[e]);
+          s[64 + e] = __uint_as_float(r2[e]);
+          s[96 + e] = __uint_as_float(r3[e]);
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(bar_f + bsel);  // S buffer may be overwritten now
+      if (t * 128 + 128 > first_invalid) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (t * 128 + c >= first_invalid) s[c] = -INFINITY;
+      }
+      // R: per key-block max (Alg. 3 l.12/l.15), stored in the scaled log2 domain
+      uint32_t rv[G];
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float gm = s[g * KK];
+#pragma unroll
+        for (int c = 1; c < KK; ++c) gm = fmaxf(gm, s[g * KK + c]);
+        tmax = fmaxf(tmax, gm);
+        rv[g] = __float_as_uint(gm * scale_log2);
+      }
+      if constexpr (G == 8) {
+        tc::st_32x32b_x8(tmem + lane_base + 256 + t * G, reinterpret_cast<uint32_t(&)[8]>(rv));
+      } else {
+        tc::st_32x32b_x4(tmem + lane_base + 256 + t * G, reinterpret_cast<uint32_t(&)[4]>(rv));
+      }
+      // online row max / sum (l.13-15)
+      const float m_new = fmaxf(m_run, tmax * scale_log2);
+      float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) {
+        acc0 += ex2(fmaf(s[c], scale_log2, -m_new));
+        acc1 += ex2(fmaf(s[c + 1], scale_log2, -m_new));
+      }
+      l_run = l_run * ex2(m_run - m_new) + (acc0 + acc1);
+      m_run = m_new;
+    }
+    tc::wait_st();
+    // pooling (l.17-19): rows of query block i are KK consecutive lanes
+    const int gr = row0 + warp * 32 + lane;
+    const int ib = gr / KK;
+    const bool row_ok = gr < NK && (gr % KK) < min(KK, N - ib * b);
+    const float inv_l = 1.f / l_run;
+    for (int j0 = 0; j0 < Nb; j0 += 32) {
+      uint32_t r[32];
+      tc::ld_32x32b_x32(tmem + lane_base + 256 + j0, r);
+      tc::wait_ld();
+      float p[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        float v = row_ok ? ex2(__uint_as_float(r[e]) - m_run) * inv_l : 0.f;
+#pragma unroll
+        for (int o = 1; o < KK; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        p[e] = v;
+      }
+      if ((lane % KK) == 0 && ib < Nb) {
+        float* dst = pimp + (u * Nb + ib) * int64_t(Nb) + j0;
+        const int nj = min(32, Nb - j0);
+        if (nj == 32 && (Nb % 4) == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(dst + e) = make_float4(p[e], p[e + 1], p[e + 2], p[e + 3]);
+        } else {
+          for (int e = 0; e < nj; ++e) dst[e] = p[e];
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 4) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int D, int KK>
+cudaError_t launch_dk(int64_t BH, int N, int Nb, int b, float scale, const void* qs,
+                      const void* ks, float* pimp, cudaStream_t stream) {
+  CUtensorMap mq, mk;
+  const int64_t NK = int64_t(Nb) * KK;
+  if (!make_tile_map(&mq, qs, BH, NK, D) || !make_tile_map(&mk, ks, BH, NK, D))
+    return cudaErrorNotSupported;
+  constexpr int smem = PCfg<D>::kSmem;
+  cudaError_t e = cudaFuncSetAttribute(probe_tc_kernel<D, KK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(unsigned((NK + 127) / 128), unsigned(BH));
+  probe_tc_kernel<D, KK><<<grid, kPThreads, smem, stream>>>(mq, mk, N, Nb, b, scale * kLog2e,
+                                                            pimp);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool probe_tc_supported(int d, int kk, int Nb) {
+  return (d == 64 || d == 128) && (kk == 16 || kk == 32) && Nb <= 256;
+}
+
+cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
+                            const void* qs, const void* ks, float* pimp, cudaStream_t stream) {
+  if (d == 128 && kk == 16) return launch_dk<128, 16>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+  if (d == 128 && kk == 32) return launch_dk<128, 32>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+  if (d == 64 && kk == 16) return launch_dk<64, 16>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+  if (d == 64 && kk == 32) return launch_dk<64, 32>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace blade
