@@ -27,6 +27,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+if os.environ.get("BLADE_DEBUG") == "1":  # hang watchdog + progress trace in attn_tc
+    FLAGS += ["-DBLADE_TC_DEBUG"]
+    OBJDIR = os.path.join(ROOT, "build", "obj_debug")
+    LIB = os.path.join(LIBDIR, "libblade_asa_debug.so")
 
 
 def _deps() -> list[str]:
@@ -56,7 +60,7 @@ def build(verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+    if True:  # linking is cheap; always relink
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt",
                "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
