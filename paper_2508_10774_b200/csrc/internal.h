@@ -22,9 +22,9 @@ struct MaskProblem {
 
 // Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
 struct MaskWorkspace {
-  size_t off_qs, off_ks, off_pimp, off_counters, off_flags, off_r64, off_mpart,
+  size_t off_qs, off_ks, off_pimp, off_counters, off_flags, off_done, off_r64, off_mpart,
       off_lpart, total;
-  int nchunks;  // refine key chunks of 256 sampled keys
+  int nchunks;  // refine key chunks of 128 sampled keys
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -33,13 +33,14 @@ inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   MaskWorkspace w{};
   const size_t rows = size_t(p.BH) * p.Nb;            // (unit, q-block) rows
   const size_t nk = size_t(p.Nb) * p.kk;              // padded sampled rows / unit
-  w.nchunks = int((nk + 255) / 256);
+  w.nchunks = int((nk + 127) / 128);
   size_t o = 0;
   w.off_qs = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);
   w.off_ks = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);
   w.off_pimp = o;     o = align256(o + rows * p.Nb * 4);
   w.off_counters = o; o = align256(o + 64);
   w.off_flags = o;    o = align256(o + rows * 4);
+  w.off_done = o;     o = align256(o + rows * 4);
   w.off_r64 = o;      o = align256(o + rows * p.kk * p.Nb * 8);
   w.off_mpart = o;    o = align256(o + rows * w.nchunks * p.kk * 8);
   w.off_lpart = o;    o = align256(o + rows * w.nchunks * p.kk * 8);
@@ -52,9 +53,23 @@ cudaError_t launch_mask(const MaskProblem& p, const void* q, const void* k, uint
                         int32_t* sample_idx, int32_t* n_refined, char* ws,
                         cudaStream_t stream);
 
+// Selection fused into the tcgen05 probe's epilogue (K-mask.3).
+struct ProbeSelect {
+  double tau;
+  int lo, hi;
+  double guard;
+  uint8_t* mask;
+  int32_t* kv_idx;
+  int32_t* kv_cnt;
+  int* counters;
+  int32_t* flags;
+  int* done;
+};
+
 bool probe_tc_supported(int d, int kk, int Nb);
 cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
-                            const void* qs, const void* ks, float* pimp, cudaStream_t stream);
+                            const void* qs, const void* ks, float* pimp, const ProbeSelect* sel,
+                            cudaStream_t stream);
 
 struct AttnProblem {
   int64_t BH;

@@ -8,13 +8,15 @@
 //            S = Q_s K_s^T on tensor cores, streaming row max M / row sum l
 //            over all N_k sampled keys, the per-(row, key-block) max R, then
 //            P_imp[i, j] = max_{s in block i} e^{R_sj - M_s} / l_s (Alg. 3).
-//   K-mask.3 select_kernel         A7-A8: one warp per (unit, q-block) row:
-//            fp64 normalisation, bitonic sort (p desc, id asc), warp scan,
-//            cut at tau, clamp, compaction to kv_idx / kv_cnt / mask.  Rows
-//            whose decision margin is within the guard band of the fp32
-//            probe error are queued for K-mask.4.
-//   K-mask.4 refine_partial/final  the queued rows' P_imp recomputed in
-//            fp64 on CUDA cores from the same sampled rows, then reselected
+//   K-mask.3 selection (select.cuh)    A7-A8: one warp per (unit, q-block)
+//            row: fp64 normalisation, register bitonic sort (p desc, id
+//            asc), warp scan, cut at tau, clamp, compaction to kv_idx /
+//            kv_cnt / mask.  Runs in the tcgen05 probe's epilogue (or as
+//            select_kernel after the mma.sync fallback probe).  Rows whose
+//            decision margin is inside the guard band of the fp32 probe
+//            error are queued for K-mask.4.
+//   K-mask.4 refine_kernel         the queued rows' P_imp recomputed in fp64
+//            on CUDA cores from the same sampled rows, then reselected
 //            (reading R-14: decisions outside the 1e-6 tie band are exact).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -23,6 +25,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "select.cuh"
 
 namespace blade {
 namespace {
@@ -60,34 +63,71 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
     const int wh = share_qk ? 0 : which;
     const uint64_t key =
         smix(smix(smix(seed, uint64_t(unit_offset + u)), uint64_t(i)), uint64_t(wh));
+    // bitonic sort of the 128 (hash, offset) pairs, ascending; 4 per lane at
+    // positions x = 4*lane + e; invalid offsets carry the maximal hash and
+    // their (larger) offset, so they sort after every valid one
     uint64_t r[4];
+    int o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int o = lane + 32 * e;
-      r[e] = o < valid ? smix(key, uint64_t(o)) : ~0ull;
+      o[e] = lane * 4 + e;
+      r[e] = o[e] < valid ? smix(key, uint64_t(o[e])) : ~0ull;
     }
-    // rank of (r, o) among all valid offsets; keep rank < ki
-    int rank[4] = {0, 0, 0, 0};
-    for (int e2 = 0; e2 < 4; ++e2) {
-      for (int src = 0; src < 32; ++src) {
-        const int o2 = src + 32 * e2;
-        const uint64_t r2 = __shfl_sync(0xffffffffu, r[e2], src);
-        if (o2 >= valid) continue;  // warp-uniform
+    auto less = [](uint64_t ra, int oa, uint64_t rb, int ob) {
+      return ra < rb || (ra == rb && oa < ob);
+    };
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int o = lane + 32 * e;
-          rank[e] += (r2 < r[e] || (r2 == r[e] && o2 < o)) ? 1 : 0;
+    for (int kb = 2; kb <= 128; kb <<= 1) {
+#pragma unroll
+      for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+        if (jb < 4) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int pe = e ^ jb;
+            if (pe > e) {
+              const bool up = ((lane * 4 + e) & kb) == 0;
+              const bool sw = up ? less(r[pe], o[pe], r[e], o[e]) : less(r[e], o[e], r[pe], o[pe]);
+              if (sw) {
+                const uint64_t tr = r[e]; r[e] = r[pe]; r[pe] = tr;
+                const int to = o[e]; o[e] = o[pe]; o[pe] = to;
+              }
+            }
+          }
+        } else {
+          const int lm = jb >> 2;
+          const bool lower = (lane & lm) == 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint64_t orr = __shfl_xor_sync(0xffffffffu, r[e], lm);
+            const int oo = __shfl_xor_sync(0xffffffffu, o[e], lm);
+            const bool up = ((lane * 4 + e) & kb) == 0;
+            const bool mine_first = less(r[e], o[e], orr, oo);
+            if (mine_first != (lower == up)) {
+              r[e] = orr;
+              o[e] = oo;
+            }
+          }
         }
       }
     }
-    int base = 0;
+    // the k_i smallest sit at positions 0..k_i-1; emit their offsets ascending
+    __shared__ uint32_t sel_bits[8][4];
+    if (lane < 4) sel_bits[warp][lane] = 0u;
+    __syncwarp();
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int o = lane + 32 * e;
-      const bool sel = o < valid && rank[e] < ki;
-      const unsigned bits = __ballot_sync(0xffffffffu, sel);
-      if (sel) offs[warp][base + __popc(bits & ((1u << lane) - 1u))] = o;
-      base += __popc(bits);
+    for (int e = 0; e < 4; ++e)
+      if (lane * 4 + e < ki) atomicOr(&sel_bits[warp][o[e] >> 5], 1u << (o[e] & 31));
+    __syncwarp();
+    if (lane == 0) {
+      int pos = 0;
+      for (int w = 0; w < 4; ++w) {
+        uint32_t bits = sel_bits[warp][w];
+        while (bits) {
+          const int bb = __ffs(bits) - 1;
+          bits &= bits - 1;
+          offs[warp][pos++] = w * 32 + bb;
+        }
+      }
     }
   }
   __syncwarp();
@@ -270,280 +310,171 @@ __global__ void __launch_bounds__(128) probe_kernel(const __nv_bfloat16* __restr
 }
 
 // ---------------------------------------------------------------------------
-// K-mask.3 / K-mask.4 shared selection (one warp, fp64; Alg. 1 l.7-10)
+// K-mask.3  selection (fallback path: after the mma.sync probe; the tcgen05
+// probe selects its own rows in its epilogue).  One warp per row.
 // ---------------------------------------------------------------------------
-struct SelScratch {
-  double val[kMaxNb];
-  int id[kMaxNb];
-  uint8_t keep[kMaxNb];
-};
-
-BLADE_DEVINL bool sel_before(double va, int ia, double vb, int ib) {
-  return va > vb || (va == vb && ia < ib);
-}
-
-// val[0:Nb) holds the raw P_imp row in fp64.  Writes the row's outputs and
-// returns true when the decision margin is inside the guard band.
-__device__ bool select_row_warp(SelScratch& sc, int Nb, double tau, int lo, int hi,
-                                double guard, bool want_flag, uint8_t* mask_row,
-                                int32_t* kv_idx_row, int32_t* kv_cnt_out) {
-  const int lane = threadIdx.x & 31;
-  int P2 = 32;
-  while (P2 < Nb) P2 <<= 1;
-  // l.7 normalise (Z summed lane-strided, then a fixed xor tree)
-  double z = 0.0;
-  for (int j = lane; j < Nb; j += 32) z += sc.val[j];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-  for (int j = lane; j < P2; j += 32) {
-    sc.val[j] = j < Nb ? sc.val[j] / z : -1.0;
-    sc.id[j] = j;
-  }
-  __syncwarp();
-  // l.8 bitonic sort: p-hat descending, ties by ascending block id (R-7)
-  for (int kb = 2; kb <= P2; kb <<= 1) {
-    for (int jb = kb >> 1; jb > 0; jb >>= 1) {
-      for (int x = lane; x < P2; x += 32) {
-        const int y = x ^ jb;
-        if (y > x) {
-          const double vx = sc.val[x], vy = sc.val[y];
-          const int ix = sc.id[x], iy = sc.id[y];
-          const bool up = (x & kb) == 0;
-          const bool swap = up ? sel_before(vy, iy, vx, ix) : sel_before(vx, ix, vy, iy);
-          if (swap) {
-            sc.val[x] = vy; sc.val[y] = vx;
-            sc.id[x] = iy;  sc.id[y] = ix;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-  // l.9 cumulative sums C_r (r = 1..Nb): per-lane segments + warp scan
-  const int seg = P2 / 32;
-  const int r0 = lane * seg;
-  double part = 0.0;
-  for (int r = r0; r < r0 + seg && r < Nb; ++r) part += sc.val[r];
-  double incl = part;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  double run = incl - part;  // exclusive prefix
-  int first = Nb + 1;
-  for (int r = r0; r < r0 + seg && r < Nb; ++r) {
-    run += sc.val[r];
-    if (run >= tau && first > Nb) first = r + 1;
-    sc.val[r] = run;  // reuse val as C_r (sorted p recoverable as differences)
-  }
-  // keep the sorted p-hat beside C: recompute from differences when needed
-#pragma unroll
-  for (int o = 16; o; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-  __syncwarp();
-  const int m0 = first <= Nb ? first : Nb;
-  const int m = min(max(m0, lo), hi);
-
-  bool flag = false;
-  if (want_flag && lane == 0) {
-    auto C = [&](int r) { return r <= 0 ? 0.0 : sc.val[r - 1]; };
-    auto clampi = [&](int x) { return min(max(x, lo), hi); };
-    const double band = guard * tau;
-    const bool cut_matters = clampi(m0 - 1) != m || clampi(m0 + 1) != m;
-    if (cut_matters && (fabs(C(m0) - tau) <= band || (m0 >= 2 && fabs(C(m0 - 1) - tau) <= band)))
-      flag = true;
-    if (m < Nb) {
-      const double pm = C(m) - C(m - 1), pn = C(m + 1) - C(m);
-      if (pm - pn <= guard * pm) flag = true;
-    }
-  }
-  flag = __shfl_sync(0xffffffffu, flag ? 1 : 0, 0) != 0;
-  // l.10 mask row + compaction (kept ids ascending)
-  for (int j = lane; j < Nb; j += 32) sc.keep[j] = 0;
-  __syncwarp();
-  for (int r = lane; r < m; r += 32) sc.keep[sc.id[r]] = 1;
-  __syncwarp();
-  int base = 0;
-  for (int j0 = 0; j0 < Nb; j0 += 32) {
-    const int j = j0 + lane;
-    const bool kp = j < Nb && sc.keep[j];
-    const unsigned bits = __ballot_sync(0xffffffffu, kp);
-    if (kp) kv_idx_row[base + __popc(bits & ((1u << lane) - 1u))] = j;
-    if (mask_row && j < Nb) mask_row[j] = kp ? 1 : 0;
-    base += __popc(bits);
-  }
-  for (int r = m + lane; r < Nb; r += 32) kv_idx_row[r] = -1;
-  if (lane == 0) *kv_cnt_out = m;
-  __syncwarp();
-  return flag;
-}
-
 constexpr int SEL_WARPS = 4;
 
 __global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(
     const float* __restrict__ pimp, int64_t rows, int Nb, double tau, int lo, int hi,
     double guard, uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx,
-    int32_t* __restrict__ kv_cnt, int* __restrict__ counters, int32_t* __restrict__ flags) {
-  extern __shared__ __align__(128) char smem[];
-  SelScratch& sc = reinterpret_cast<SelScratch*>(smem)[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  const int64_t row = int64_t(blockIdx.x) * SEL_WARPS + (threadIdx.x >> 5);
+    int32_t* __restrict__ kv_cnt, int* __restrict__ counters, int32_t* __restrict__ flags,
+    int* __restrict__ done) {
+  __shared__ uint32_t keep_bits[SEL_WARPS][16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * SEL_WARPS + warp;
   if (row >= rows) return;
-  const float* src = pimp + row * Nb;
-  for (int j = lane; j < Nb; j += 32) sc.val[j] = double(src[j]);
-  __syncwarp();
-  const bool flag = select_row_warp(sc, Nb, tau, lo, hi, guard, true,
-                                    mask ? mask + row * Nb : nullptr, kv_idx + row * Nb,
-                                    kv_cnt + row);
+  const bool flag = select_row(pimp + row * Nb, Nb, tau, lo, hi, guard, true,
+                               mask ? mask + row * Nb : nullptr, kv_idx + row * Nb, kv_cnt + row,
+                               keep_bits[warp]);
   if (flag && lane == 0) {
     const int slot = atomicAdd(&counters[0], 1);
     flags[slot] = int32_t(row);
+    done[slot] = 0;
   }
 }
 
 // ---------------------------------------------------------------------------
-// K-mask.4a  fp64 partial probe of queued rows: one CTA per (queued row,
-// chunk of 256 sampled keys).  Thread t owns one sampled key; logits for 16
-// query rows at a time are exact-product fp64 dot products.
+// K-mask.4  fp64 recomputation of queued rows.  One CTA (128 threads) per
+// (queued row, chunk of 128 sampled keys): thread t owns one sampled key and
+// forms the exact-product fp64 logits against the row's k_i sampled queries,
+// 16 at a time; per chunk it leaves R (per key block), the chunk max M_c and
+// l_c = sum exp(L - M_c).  The CTA that finishes a row's last chunk combines
+// them (Alg. 3 l.14: M = max M_c, l = sum l_c e^{M_c - M}), forms the fp64
+// P_imp row (l.17-19) and reselects it.  The reselection sorts the fp64
+// values rounded to fp32 (relative error 6e-8, far inside the 1e-6 tie band).
 // ---------------------------------------------------------------------------
+constexpr int RF_KEYS = 128;
+
 template <int D>
-__global__ void __launch_bounds__(256) refine_partial_kernel(
-    const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N,
-    int Nb, int b, int kk, double scale, int nchunks, const int* __restrict__ counters,
-    const int32_t* __restrict__ flags, double* __restrict__ r64, double* __restrict__ mpart,
-    double* __restrict__ lpart) {
-  __shared__ double sq[16][D];
-  __shared__ double sRg[16][16];   // [16-key group][s] group max
+__global__ void __launch_bounds__(RF_KEYS, 3) refine_kernel(
+    const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N, int Nb,
+    int b, int kk, double scale, int nchunks, double tau, int lo, int hi,
+    const int* __restrict__ counters, const int32_t* __restrict__ flags, int* __restrict__ done,
+    double* __restrict__ r64, double* __restrict__ mpart, double* __restrict__ lpart,
+    float* __restrict__ pimp_out, uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx,
+    int32_t* __restrict__ kv_cnt, int32_t* __restrict__ n_refined) {
+  __shared__ __align__(16) double sq[D][16];   // [d][s]: one LDS.128 serves two query rows
+  __shared__ double sRg[8][16];                // [16-key group][s] group max
+  __shared__ double sW[4][16];                 // per-warp partials
   __shared__ double sMc[16];
-  __shared__ double sLw[8][16];
+  __shared__ float sRow[kMaxNb];
+  __shared__ double sMs[128], sLs[128];
+  __shared__ uint32_t keep_bits[16];
+  __shared__ int last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nflag = counters[0];
+  if (blockIdx.x == 0 && tid == 0 && n_refined) *n_refined = nflag;
   const int NK = Nb * kk;
-  const int G = kk < 16 ? kk : 16;  // keys per reduction group (kk >= 16 here)
   for (int item = blockIdx.x; item < nflag * nchunks; item += gridDim.x) {
     const int f = item / nchunks, c = item % nchunks;
     const int64_t row = flags[f];
     const int64_t u = row / Nb;
     const int i = int(row % Nb);
     const int ki = min(kk, min(b, N - i * b));
-    const int key = c * 256 + tid;
+    const int key = c * RF_KEYS + tid;
     const int jb = key / kk, rr = key - jb * kk;
     const bool kvalid = key < NK && rr < min(kk, min(b, N - jb * b));
     const __nv_bfloat16* kp = ks + (u * NK + min(key, NK - 1)) * int64_t(D);
     for (int sg = 0; sg < kk; sg += 16) {
       __syncthreads();
-      for (int e = tid; e < 16 * D; e += 256) {
-        const int s = e / D, dd = e % D;
-        sq[s][dd] = double(__bfloat162float(qs[(u * NK + int64_t(i) * kk + sg + s) * D + dd]));
+      for (int e = tid; e < 16 * D; e += RF_KEYS) {
+        const int sq_s = e & 15, dd = e >> 4;
+        sq[dd][sq_s] =
+            double(__bfloat162float(qs[(u * NK + int64_t(i) * kk + sg + sq_s) * D + dd]));
       }
       __syncthreads();
       double L[16];
 #pragma unroll
-      for (int s = 0; s < 16; ++s) L[s] = 0.0;
+      for (int q = 0; q < 16; ++q) L[q] = 0.0;
+#pragma unroll 1
       for (int d0 = 0; d0 < D; d0 += 8) {
         const uint4 raw = *reinterpret_cast<const uint4*>(kp + d0);
         const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
-        double kv[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) kv[e] = double(__bfloat162float(h[e]));
+        for (int e = 0; e < 8; ++e) {
+          const double kv = double(__bfloat162float(h[e]));
 #pragma unroll
-        for (int s = 0; s < 16; ++s)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) L[s] = fma(sq[s][d0 + e], kv[e], L[s]);
+          for (int q = 0; q < 16; q += 2) {
+            const double2 qq = *reinterpret_cast<const double2*>(&sq[d0 + e][q]);
+            L[q] = fma(qq.x, kv, L[q]);
+            L[q + 1] = fma(qq.y, kv, L[q + 1]);
+          }
+        }
       }
 #pragma unroll
-      for (int s = 0; s < 16; ++s) L[s] = kvalid ? L[s] * scale : -INFINITY;
-      // R: max over each group of 16 consecutive keys (a key block for k=16)
+      for (int q = 0; q < 16; ++q) L[q] = kvalid ? L[q] * scale : -INFINITY;
+      // per 16-key group max (a key block when kk = 16)
 #pragma unroll
-      for (int s = 0; s < 16; ++s) {
-        double v = L[s];
+      for (int q = 0; q < 16; ++q) {
+        double v = L[q];
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if ((lane & 15) == 0) sRg[tid >> 4][s] = v;
+        if ((lane & 15) == 0) sRg[tid >> 4][q] = v;
       }
       __syncthreads();
-      // combine groups into key blocks, store R, and the chunk max per s
-      const int gpb = kk / G;  // groups per key block
-      const int nblk = 256 / kk;
+      const int gpb = kk / 16;          // 16-key groups per key block
+      const int nblk = RF_KEYS / kk;    // key blocks per chunk (kk <= 128)
       if (tid < 16 * nblk) {
-        const int s = tid & 15, bl = tid >> 4;
+        const int q = tid & 15, bl = tid >> 4;
         double v = -INFINITY;
-        for (int gg = 0; gg < gpb; ++gg) v = fmax(v, sRg[bl * gpb + gg][s]);
+        for (int gg = 0; gg < gpb; ++gg) v = fmax(v, sRg[bl * gpb + gg][q]);
         const int j = c * nblk + bl;
-        if (j < Nb && sg + s < ki) r64[(int64_t(f) * kk + sg + s) * Nb + j] = v;
+        if (j < Nb && sg + q < ki) r64[(int64_t(f) * kk + sg + q) * Nb + j] = v;
       }
       if (tid < 16) {
         double v = -INFINITY;
-        for (int gg = 0; gg < 16; ++gg) v = fmax(v, sRg[gg][tid]);
+        for (int gg = 0; gg < 8; ++gg) v = fmax(v, sRg[gg][tid]);
         sMc[tid] = v;
       }
       __syncthreads();
 #pragma unroll
-      for (int s = 0; s < 16; ++s) {
-        double e = (L[s] == -INFINITY) ? 0.0 : exp(L[s] - sMc[s]);
+      for (int q = 0; q < 16; ++q) {
+        double e = (L[q] == -INFINITY) ? 0.0 : exp(L[q] - sMc[q]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if (lane == 0) sLw[warp][s] = e;
+        if (lane == 0) sW[warp][q] = e;
       }
       __syncthreads();
       if (tid < 16 && sg + tid < ki) {
-        double l = 0.0;
-        for (int ww = 0; ww < 8; ++ww) l += sLw[ww][tid];
+        const double l = sW[0][tid] + sW[1][tid] + sW[2][tid] + sW[3][tid];
         const int64_t o = (int64_t(f) * nchunks + c) * kk + sg + tid;
         mpart[o] = sMc[tid];
         lpart[o] = l;
       }
     }
-  }
-}
-
-// K-mask.4b  combine the partials of each queued row into its fp64 P_imp row
-// (Alg. 3 l.14, l.17-19) and reselect it.  One CTA per queued row: threads
-// own query rows for the combine, key blocks for the max-pool, then warp 0
-// reruns the selection on the fp64 row.
-constexpr int RF_THREADS = 256;
-
-__global__ void __launch_bounds__(RF_THREADS) refine_final_kernel(
-    int Nb, int N, int b, int kk, int nchunks, double tau, int lo, int hi,
-    const int* __restrict__ counters, const int32_t* __restrict__ flags,
-    const double* __restrict__ r64, const double* __restrict__ mpart,
-    const double* __restrict__ lpart, float* __restrict__ pimp, uint8_t* __restrict__ mask,
-    int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt, int32_t* n_refined) {
-  extern __shared__ __align__(128) char smem[];
-  SelScratch& sc = *reinterpret_cast<SelScratch*>(smem);
-  double* sMs = reinterpret_cast<double*>(smem + sizeof(SelScratch));
-  double* sLs = sMs + 128;
-  const int tid = threadIdx.x;
-  const int nflag = counters[0];
-  if (blockIdx.x == 0 && tid == 0 && n_refined) *n_refined = nflag;
-  for (int f = blockIdx.x; f < nflag; f += gridDim.x) {
-    const int64_t row = flags[f];
-    const int i = int(row % Nb);
-    const int ki = min(kk, min(b, N - i * b));
+    // ---- last chunk of this row: combine and reselect ----
+    __threadfence();
     __syncthreads();
+    if (tid == 0) last = (atomicAdd(&done[f], 1) == nchunks - 1);
+    __syncthreads();
+    if (!last) continue;
+    __threadfence();
     if (tid < ki) {
       double M = -INFINITY;
-      for (int c = 0; c < nchunks; ++c) M = fmax(M, mpart[(int64_t(f) * nchunks + c) * kk + tid]);
+      for (int cc = 0; cc < nchunks; ++cc)
+        M = fmax(M, __ldcg(&mpart[(int64_t(f) * nchunks + cc) * kk + tid]));
       double l = 0.0;
-      for (int c = 0; c < nchunks; ++c) {
-        const int64_t o = (int64_t(f) * nchunks + c) * kk + tid;
-        if (mpart[o] != -INFINITY) l += lpart[o] * exp(mpart[o] - M);
+      for (int cc = 0; cc < nchunks; ++cc) {
+        const int64_t o = (int64_t(f) * nchunks + cc) * kk + tid;
+        const double mc = __ldcg(&mpart[o]);
+        if (mc != -INFINITY) l += __ldcg(&lpart[o]) * exp(mc - M);
       }
       sMs[tid] = M;
-      sLs[tid] = l;
+      sLs[tid] = 1.0 / l;
     }
     __syncthreads();
-    for (int j = tid; j < Nb; j += RF_THREADS) {
+    for (int j = tid; j < Nb; j += RF_KEYS) {
       double best = 0.0;
-      for (int s = 0; s < ki; ++s)
-        best = fmax(best, exp(r64[(int64_t(f) * kk + s) * Nb + j] - sMs[s]) / sLs[s]);
-      sc.val[j] = best;
-      if (pimp) pimp[row * Nb + j] = float(best);
+      for (int q = 0; q < ki; ++q)
+        best = fmax(best, exp(__ldcg(&r64[(int64_t(f) * kk + q) * Nb + j]) - sMs[q]) * sLs[q]);
+      sRow[j] = float(best);
+      if (pimp_out) pimp_out[row * Nb + j] = float(best);
     }
     __syncthreads();
-    if (tid < 32)
-      select_row_warp(sc, Nb, tau, lo, hi, 0.0, false, mask ? mask + row * Nb : nullptr,
-                      kv_idx + row * Nb, kv_cnt + row);
+    if (warp == 0)
+      select_row(static_cast<const float*>(sRow), Nb, tau, lo, hi, 0.0, false,
+                 mask ? mask + row * Nb : nullptr, kv_idx + row * Nb, kv_cnt + row, keep_bits);
   }
 }
 
@@ -558,10 +489,12 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   float* pimp = p_imp_out ? p_imp_out : reinterpret_cast<float*>(ws + w.off_pimp);
   int* counters = reinterpret_cast<int*>(ws + w.off_counters);
   int32_t* flags = reinterpret_cast<int32_t*>(ws + w.off_flags);
+  int* done = reinterpret_cast<int*>(ws + w.off_done);
   double* r64 = reinterpret_cast<double*>(ws + w.off_r64);
   double* mpart = reinterpret_cast<double*>(ws + w.off_mpart);
   double* lpart = reinterpret_cast<double*>(ws + w.off_lpart);
   const int64_t rows = p.BH * p.Nb;
+  cudaError_t e;
 
   {  // K-mask.1
     const int64_t warps = p.BH * p.Nb * 2;
@@ -570,44 +503,32 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
         ks, counters);
   }
-  if (probe_tc_supported(D, p.kk, p.Nb)) {  // K-mask.2 on tcgen05 (k in {16, 32}, N_b <= 256)
-    cudaError_t e = launch_probe_tc(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
+  if (probe_tc_supported(D, p.kk, p.Nb)) {
+    // K-mask.2 + K-mask.3 fused: tcgen05 probe, selection in its epilogue
+    ProbeSelect ps{p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done};
+    e = launch_probe_tc(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, &ps, stream);
     if (e != cudaSuccess) return e;
   } else {
-  if (p.kk > PR_ROWS) {
-    cudaError_t e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);
-    if (e != cudaSuccess) return e;
-  }
-  {  // K-mask.2 (mma.sync fallback for other k / longer sequences)
+    if (p.kk > PR_ROWS) {
+      e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);
+      if (e != cudaSuccess) return e;
+    }
     const size_t smem = size_t(PR_ROWS) * D * 2 + 2 * PR_KEYS * D * 2 +
                         size_t(PR_ROWS) * p.Nb * 4 + 2 * PR_ROWS * 4;
-    cudaError_t e = cudaFuncSetAttribute(probe_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    e = cudaFuncSetAttribute(probe_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
     if (e != cudaSuccess) return e;
     dim3 grid(unsigned((p.Nb * p.kk + PR_ROWS - 1) / PR_ROWS), unsigned(p.BH));
-    probe_kernel<D><<<grid, 128, smem, stream>>>(qs, ks, p.N, p.Nb, p.b, p.kk,
-                                                 p.scale * kLog2e, pimp);
+    probe_kernel<D><<<grid, 128, smem, stream>>>(qs, ks, p.N, p.Nb, p.b, p.kk, p.scale * kLog2e,
+                                                 pimp);
+    select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
+        pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
+        done);
   }
-  }
-  const size_t sel_smem = SEL_WARPS * sizeof(SelScratch);
-  {  // K-mask.3
-    cudaError_t e = cudaFuncSetAttribute(select_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sel_smem));
-    if (e != cudaSuccess) return e;
-    select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, sel_smem,
-                    stream>>>(pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt,
-                              counters, flags);
-  }
-  {  // K-mask.4 (persistent grids; the queue length is read on the device)
-    refine_partial_kernel<D><<<148 * 4, 256, 0, stream>>>(
-        qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, counters, flags, r64, mpart,
-        lpart);
-    const size_t fsmem = sizeof(SelScratch) + 256 * sizeof(double);
-    refine_final_kernel<<<148, RF_THREADS, fsmem, stream>>>(
-        p.Nb, p.N, p.b, p.kk, w.nchunks, p.tau, p.lo, p.hi, counters, flags, r64, mpart, lpart,
-        p_imp_out, mask, kv_idx, kv_cnt, n_refined);
-  }
+  // K-mask.4 (persistent grid; the queue length is read on the device)
+  refine_kernel<D><<<148 * 8, RF_KEYS, 0, stream>>>(
+      qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
+      flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
   return cudaGetLastError();
 }
 

@@ -4,14 +4,15 @@
 //
 // CTA = 128 sampled query rows (M = 128) of one unit, streaming every
 // 128-key tile of that unit's sampled keys K_s:
-//   warps 0-3  row statistics, thread = sampled query row = TMEM lane:
+//   warps 0-7  row statistics; two warpgroups split each 128-key tile into
+//              column halves, thread = sampled query row = TMEM lane:
 //              running max M and sum l of e^{s - M} over all sampled keys
 //              (l.12-15), and the per-(row, key-block) max R (l.15) kept in
 //              TMEM beside the S buffers; at the end
 //              P_imp[i, j] = max over the k rows of block i of e^{R - M} / l
 //              (l.17-19) with a 16/32-lane shuffle max.
-//   warp  4    tcgen05.mma issuer (S = Q_s K_s^T, double-buffered in TMEM)
-//   warp  5    TMA producer (Q_s tile once, K_s tiles through a smem ring)
+//   warp  8    tcgen05.mma issuer (S = Q_s K_s^T, double-buffered in TMEM)
+//   warp  9    TMA producer (Q_s tile once, K_s tiles through a smem ring)
 // TMEM: S0 [0,128) S1 [128,256) R [256, 256 + N_b)  (N_b <= 256).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -21,6 +22,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
+#include "select.cuh"
 #include "tma_host.h"
 
 namespace blade {
@@ -36,15 +38,16 @@ struct PCfg {
   static constexpr int kOffBar = kOffRing + kRing * kTile;
   static constexpr int kNumBar = 1 + 2 * kRing + 4;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
-  static constexpr int kSmem = kOffMisc + 16 + 1024;
+  static constexpr int kSmem = kOffMisc + 16 + 8 * 16 * 4 + 4 * 128 * 4 + 1024;
 };
 
-constexpr int kPThreads = 256;
+constexpr int kPThreads = 384;  // warps 0-7 softmax, 8 MMA, 9 TMA, 10-11 idle
 
 template <int D, int KK>
 __global__ void __launch_bounds__(kPThreads, 1)
     probe_tc_kernel(const __grid_constant__ CUtensorMap tmQs, const __grid_constant__ CUtensorMap tmKs,
-                    int N, int Nb, int b, float scale_log2, float* __restrict__ pimp) {
+                    int N, int Nb, int b, float scale_log2, float* __restrict__ pimp,
+                    const ProbeSelect sel) {
   using C = PCfg<D>;
   constexpr int G = 128 / KK;  // key blocks per 128-key tile
   extern __shared__ __align__(1024) char smem_raw[];
@@ -58,6 +61,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* bar_s = bars + 1 + 2 * C::kRing;   // [2] S buffer written
   uint64_t* bar_f = bar_s + 2;                  // [2] S buffer read out
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+  uint32_t* keep_bits = tmem_slot + 4;  // [8 warps][16]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t u = blockIdx.y;
@@ -67,7 +71,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int k_last = min(KK, N - (Nb - 1) * b);
   const int first_invalid = (Nb - 1) * KK + k_last;  // sampled columns >= this are padding
 
-  if (warp == 5 && lane == 0) {
+  if (warp == 9 && lane == 0) {
     tc::mbar_init(bar_q, 1);
     for (int s = 0; s < C::kRing; ++s) {
       tc::mbar_init(bar_full + s, 1);
@@ -75,17 +79,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       tc::mbar_init(bar_s + t, 1);
-      tc::mbar_init(bar_f + t, 128);
+      tc::mbar_init(bar_f + t, 8);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 4) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == 8) tc::tmem_alloc<512>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5) {
+  if (warp == 9) {
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmQs);
       tc::tma_prefetch_desc(&tmKs);
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                           t * 128, int(u));
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 8) {
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       const uint32_t qa = smem_u32(sQ), rb = smem_u32(sRing);
@@ -123,81 +127,97 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tc::commit(bar_empty + s);
       }
     }
-  } else if (warp < 4) {
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  } else if (warp < 8) {
+    // two warpgroups split each 128-key tile: half h owns columns [64h, 64h+64)
+    // (key blocks [h*G/2, (h+1)*G/2) of the tile) with its own running (M, l)
+    constexpr int GH = G / 2;
+    const int h = warp >> 2, quad = warp & 3;
+    const uint32_t lane_base = uint32_t(quad * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < ntiles; ++t) {
       const int bsel = t & 1;
       tc::mbar_wait(bar_s + bsel, (t >> 1) & 1);
       tc::fence_after_sync();
-      float s[128];
+      float s[64];
       {
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        const uint32_t ta = tmem + lane_base + bsel * 128;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem + lane_base + bsel * 128 + h * 64;
         tc::ld_32x32b_x32(ta + 0, r0);
         tc::ld_32x32b_x32(ta + 32, r1);
-        tc::ld_32x32b_x32(ta + 64, r2);
-        tc::ld_32x32b_x32(ta + 96, r3);
         tc::wait_ld();
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           s[e] = __uint_as_float(r0[e]);
           s[32 + e] = __uint_as_float(r1[e]);
-          s[64 + e] = __uint_as_float(r2[e]);
-          s[96 + e] = __uint_as_float(r3[e]);
         }
       }
       tc::fence_before_sync();
-      tc::mbar_arrive(bar_f + bsel);  // S buffer may be overwritten now
-      if (t * 128 + 128 > first_invalid) {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bar_f + bsel);  // S buffer may be overwritten now
+      const int col0 = t * 128 + h * 64;
+      if (col0 + 64 > first_invalid) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (t * 128 + c >= first_invalid) s[c] = -INFINITY;
+        for (int c = 0; c < 64; ++c)
+          if (col0 + c >= first_invalid) s[c] = -INFINITY;
       }
       // R: per key-block max (Alg. 3 l.12/l.15), stored in the scaled log2 domain
-      uint32_t rv[G];
+      uint32_t rv[GH];
       float tmax = -INFINITY;
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
+      for (int g = 0; g < GH; ++g) {
         float gm = s[g * KK];
 #pragma unroll
         for (int c = 1; c < KK; ++c) gm = fmaxf(gm, s[g * KK + c]);
         tmax = fmaxf(tmax, gm);
         rv[g] = __float_as_uint(gm * scale_log2);
       }
-      if constexpr (G == 8) {
-        tc::st_32x32b_x8(tmem + lane_base + 256 + t * G, reinterpret_cast<uint32_t(&)[8]>(rv));
+      const uint32_t rcol = tmem + lane_base + 256 + t * G + h * GH;
+      if constexpr (GH == 4) {
+        tc::st_32x32b_x4(rcol, reinterpret_cast<uint32_t(&)[4]>(rv));
       } else {
-        tc::st_32x32b_x4(tmem + lane_base + 256 + t * G, reinterpret_cast<uint32_t(&)[4]>(rv));
+        tc::st_32x32b_x2(rcol, reinterpret_cast<uint32_t(&)[2]>(rv));
       }
-      // online row max / sum (l.13-15)
+      // online row max / sum over this half (l.13-15)
       const float m_new = fmaxf(m_run, tmax * scale_log2);
-      float acc0 = 0.f, acc1 = 0.f;
+      if (m_new != -INFINITY) {  // a half tile of padding only leaves (M, l) untouched
+        float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        acc0 += ex2(fmaf(s[c], scale_log2, -m_new));
-        acc1 += ex2(fmaf(s[c + 1], scale_log2, -m_new));
+        for (int c = 0; c < 64; c += 2) {
+          acc0 += ex2(fmaf(s[c], scale_log2, -m_new));
+          acc1 += ex2(fmaf(s[c + 1], scale_log2, -m_new));
+        }
+        l_run = l_run * ex2(m_run - m_new) + (acc0 + acc1);
+        m_run = m_new;
       }
-      l_run = l_run * ex2(m_run - m_new) + (acc0 + acc1);
-      m_run = m_new;
     }
     tc::wait_st();
-    // pooling (l.17-19): rows of query block i are KK consecutive lanes
-    const int gr = row0 + warp * 32 + lane;
+    // merge the two halves' (M, l) per row (the l.14 recurrence, once)
+    float* sml = reinterpret_cast<float*>(keep_bits + 8 * 16);  // [2][128] m, [2][128] l
+    const int r = quad * 32 + lane;
+    sml[h * 128 + r] = m_run;
+    sml[256 + h * 128 + r] = l_run;
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    const float m0 = sml[r], m1 = sml[128 + r];
+    const float M = fmaxf(m0, m1);
+    const float L = (m0 == -INFINITY ? 0.f : sml[256 + r] * ex2(m0 - M)) +
+                    (m1 == -INFINITY ? 0.f : sml[384 + r] * ex2(m1 - M));
+    // pooling (l.17-19): rows of query block i are KK consecutive lanes; the
+    // two halves take alternate 32-column chunks of R
+    const int gr = row0 + r;
     const int ib = gr / KK;
     const bool row_ok = gr < NK && (gr % KK) < min(KK, N - ib * b);
-    const float inv_l = 1.f / l_run;
-    for (int j0 = 0; j0 < Nb; j0 += 32) {
-      uint32_t r[32];
-      tc::ld_32x32b_x32(tmem + lane_base + 256 + j0, r);
+    const float inv_l = 1.f / L;
+    for (int j0 = h * 32; j0 < Nb; j0 += 64) {
+      uint32_t rr[32];
+      tc::ld_32x32b_x32(tmem + lane_base + 256 + j0, rr);
       tc::wait_ld();
-      float p[32];
+      float pv[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        float v = row_ok ? ex2(__uint_as_float(r[e]) - m_run) * inv_l : 0.f;
+        float v = row_ok ? ex2(__uint_as_float(rr[e]) - M) * inv_l : 0.f;
 #pragma unroll
         for (int o = 1; o < KK; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        p[e] = v;
+        pv[e] = v;
       }
       if ((lane % KK) == 0 && ib < Nb) {
         float* dst = pimp + (u * Nb + ib) * int64_t(Nb) + j0;
@@ -205,16 +225,34 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (nj == 32 && (Nb % 4) == 0) {
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(dst + e) = make_float4(p[e], p[e + 1], p[e + 2], p[e + 3]);
+            *reinterpret_cast<float4*>(dst + e) = make_float4(pv[e], pv[e + 1], pv[e + 2], pv[e + 3]);
         } else {
-          for (int e = 0; e < nj; ++e) dst[e] = p[e];
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < nj) dst[e] = pv[e];
         }
       }
     }
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) {
+  // K-mask.3 fused: the CTA holds complete P_imp rows of its 128 / KK query
+  // blocks; one warp selects each (Alg. 1 l.7-10, select.cuh)
+  {
+    const int ib = row0 / KK + warp;
+    if (warp < 128 / KK && ib < Nb) {
+      const int64_t row = u * Nb + ib;
+      const bool flag = select_row(pimp + row * Nb, Nb, sel.tau, sel.lo, sel.hi, sel.guard, true,
+                                   sel.mask ? sel.mask + row * Nb : nullptr,
+                                   sel.kv_idx + row * Nb, sel.kv_cnt + row, keep_bits + warp * 16);
+      if (flag && lane == 0) {
+        const int slot = atomicAdd(&sel.counters[0], 1);
+        sel.flags[slot] = int32_t(row);
+        sel.done[slot] = 0;
+      }
+    }
+  }
+  if (warp == 8) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
   }
@@ -222,7 +260,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
 template <int D, int KK>
 cudaError_t launch_dk(int64_t BH, int N, int Nb, int b, float scale, const void* qs,
-                      const void* ks, float* pimp, cudaStream_t stream) {
+                      const void* ks, float* pimp, const ProbeSelect& sel, cudaStream_t stream) {
   CUtensorMap mq, mk;
   const int64_t NK = int64_t(Nb) * KK;
   if (!make_tile_map(&mq, qs, BH, NK, D) || !make_tile_map(&mk, ks, BH, NK, D))
@@ -233,7 +271,7 @@ cudaError_t launch_dk(int64_t BH, int N, int Nb, int b, float scale, const void*
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned((NK + 127) / 128), unsigned(BH));
   probe_tc_kernel<D, KK><<<grid, kPThreads, smem, stream>>>(mq, mk, N, Nb, b, scale * kLog2e,
-                                                            pimp);
+                                                            pimp, sel);
   return cudaGetLastError();
 }
 
@@ -244,11 +282,12 @@ bool probe_tc_supported(int d, int kk, int Nb) {
 }
 
 cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
-                            const void* qs, const void* ks, float* pimp, cudaStream_t stream) {
-  if (d == 128 && kk == 16) return launch_dk<128, 16>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
-  if (d == 128 && kk == 32) return launch_dk<128, 32>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
-  if (d == 64 && kk == 16) return launch_dk<64, 16>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
-  if (d == 64 && kk == 32) return launch_dk<64, 32>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+                            const void* qs, const void* ks, float* pimp, const ProbeSelect* sel,
+                            cudaStream_t stream) {
+  if (d == 128 && kk == 16) return launch_dk<128, 16>(BH, N, Nb, b, scale, qs, ks, pimp, *sel, stream);
+  if (d == 128 && kk == 32) return launch_dk<128, 32>(BH, N, Nb, b, scale, qs, ks, pimp, *sel, stream);
+  if (d == 64 && kk == 16) return launch_dk<64, 16>(BH, N, Nb, b, scale, qs, ks, pimp, *sel, stream);
+  if (d == 64 && kk == 32) return launch_dk<64, 32>(BH, N, Nb, b, scale, qs, ks, pimp, *sel, stream);
   return cudaErrorNotSupported;
 }
 

@@ -141,6 +141,11 @@ BLADE_DEVINL void st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
                "r"(r[7])
                : "memory");
 }
+BLADE_DEVINL void st_32x32b_x2(uint32_t taddr, const uint32_t (&r)[2]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};\n" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1])
+               : "memory");
+}
 BLADE_DEVINL void st_32x32b_x4(uint32_t taddr, const uint32_t (&r)[4]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr),
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
