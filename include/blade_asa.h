@@ -66,7 +66,7 @@ typedef struct {
   int32_t  share_qk;     /* 0: independent Q and K samples; 1: K reuses Q's offsets     */
   int64_t  unit_offset;  /* global index of this call's first unit (sharding, R-1)      */
   float    refine_guard; /* relative decision margin below which a row is recomputed in
-                            fp64 (reading R-14); <= 0 selects the default 2e-5          */
+                            fp64 (reading R-14); <= 0 selects the default 1e-5          */
   int32_t  reserved;     /* must be 0                                                    */
 } blade_asa_params_t;
 

@@ -48,7 +48,7 @@ blade_status_t make_mask_problem(int64_t BH, int32_t N, int32_t d,
   p.mode = prm->sample_mode;
   p.share_qk = prm->share_qk ? 1 : 0;
   p.unit_offset = prm->unit_offset;
-  p.guard = prm->refine_guard > 0.f ? double(prm->refine_guard) : 2e-5;
+  p.guard = prm->refine_guard > 0.f ? double(prm->refine_guard) : 1e-5;
   *out = p;
   return BLADE_OK;
 }

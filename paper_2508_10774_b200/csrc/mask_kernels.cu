@@ -521,9 +521,11 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     dim3 grid(unsigned((p.Nb * p.kk + PR_ROWS - 1) / PR_ROWS), unsigned(p.BH));
     probe_kernel<D><<<grid, 128, smem, stream>>>(qs, ks, p.N, p.Nb, p.b, p.kk, p.scale * kLog2e,
                                                  pimp);
+    // the fallback probe sums l sequentially in fp32 (error up to ~2e-6): never
+    // trust it inside a 2e-5 band
     select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
-        pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
-        done);
+        pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard > 2e-5 ? p.guard : 2e-5, mask, kv_idx,
+        kv_cnt, counters, flags, done);
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
   refine_kernel<D><<<148 * 8, RF_KEYS, 0, stream>>>(

@@ -38,7 +38,7 @@ struct PCfg {
   static constexpr int kOffBar = kOffRing + kRing * kTile;
   static constexpr int kNumBar = 1 + 2 * kRing + 4;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
-  static constexpr int kSmem = kOffMisc + 16 + 8 * 16 * 4 + 4 * 128 * 4 + 1024;
+  static constexpr int kSmem = kOffMisc + 16 + 8 * 16 * 4 + 2 * 128 * 4 + 2 * 128 * 8 + 1024;
 };
 
 constexpr int kPThreads = 384;  // warps 0-7 softmax, 8 MMA, 9 TMA, 10-11 idle
@@ -133,7 +133,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
     constexpr int GH = G / 2;
     const int h = warp >> 2, quad = warp & 3;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    float m_run = -INFINITY, l_run = 0.f;
+    // l is kept in fp64 across tiles and each tile's 64 terms are summed as a
+    // tree: the sequential fp32 sum over N_k terms would dominate the probe's
+    // error budget (DESIGN.md §Tie band)
+    float m_run = -INFINITY;
+    double l_run = 0.0;
     for (int t = 0; t < ntiles; ++t) {
       const int bsel = t & 1;
       tc::mbar_wait(bar_s + bsel, (t >> 1) & 1);
@@ -160,7 +164,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int c = 0; c < 64; ++c)
           if (col0 + c >= first_invalid) s[c] = -INFINITY;
       }
-      // R: per key-block max (Alg. 3 l.12/l.15), stored in the scaled log2 domain
+      // R: per key-block max of the raw logits (Alg. 3 l.12/l.15); M and R stay
+      // unscaled so every exponent is formed as (s - M) * scale once
       uint32_t rv[GH];
       float tmax = -INFINITY;
 #pragma unroll
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
         for (int c = 1; c < KK; ++c) gm = fmaxf(gm, s[g * KK + c]);
         tmax = fmaxf(tmax, gm);
-        rv[g] = __float_as_uint(gm * scale_log2);
+        rv[g] = __float_as_uint(gm);
       }
       const uint32_t rcol = tmem + lane_base + 256 + t * G + h * GH;
       if constexpr (GH == 4) {
@@ -178,35 +183,38 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tc::st_32x32b_x2(rcol, reinterpret_cast<uint32_t(&)[2]>(rv));
       }
       // online row max / sum over this half (l.13-15)
-      const float m_new = fmaxf(m_run, tmax * scale_log2);
+      const float m_new = fmaxf(m_run, tmax);
       if (m_new != -INFINITY) {  // a half tile of padding only leaves (M, l) untouched
-        float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          acc0 += ex2(fmaf(s[c], scale_log2, -m_new));
-          acc1 += ex2(fmaf(s[c + 1], scale_log2, -m_new));
-        }
-        l_run = l_run * ex2(m_run - m_new) + (acc0 + acc1);
+        for (int c = 0; c < 64; ++c) s[c] = ex2((s[c] - m_new) * scale_log2);
+#pragma unroll
+        for (int w = 32; w >= 1; w >>= 1)
+#pragma unroll
+          for (int c = 0; c < w; ++c) s[c] += s[c + w];
+        if (m_new != m_run) l_run *= exp2((double(m_run) - double(m_new)) * double(scale_log2));
+        l_run += double(s[0]);
         m_run = m_new;
       }
     }
     tc::wait_st();
     // merge the two halves' (M, l) per row (the l.14 recurrence, once)
-    float* sml = reinterpret_cast<float*>(keep_bits + 8 * 16);  // [2][128] m, [2][128] l
+    float* smm = reinterpret_cast<float*>(keep_bits + 8 * 16);        // [2][128] m
+    double* sml = reinterpret_cast<double*>(smm + 256);                 // [2][128] l
     const int r = quad * 32 + lane;
-    sml[h * 128 + r] = m_run;
-    sml[256 + h * 128 + r] = l_run;
+    smm[h * 128 + r] = m_run;
+    sml[h * 128 + r] = l_run;
     asm volatile("bar.sync 1, 256;\n" ::: "memory");
-    const float m0 = sml[r], m1 = sml[128 + r];
+    const float m0 = smm[r], m1 = smm[128 + r];
     const float M = fmaxf(m0, m1);
-    const float L = (m0 == -INFINITY ? 0.f : sml[256 + r] * ex2(m0 - M)) +
-                    (m1 == -INFINITY ? 0.f : sml[384 + r] * ex2(m1 - M));
+    const double sl2 = double(scale_log2);
+    const double L = (m0 == -INFINITY ? 0.0 : sml[r] * exp2((double(m0) - double(M)) * sl2)) +
+                     (m1 == -INFINITY ? 0.0 : sml[128 + r] * exp2((double(m1) - double(M)) * sl2));
     // pooling (l.17-19): rows of query block i are KK consecutive lanes; the
     // two halves take alternate 32-column chunks of R
     const int gr = row0 + r;
     const int ib = gr / KK;
     const bool row_ok = gr < NK && (gr % KK) < min(KK, N - ib * b);
-    const float inv_l = 1.f / L;
+    const float inv_l = float(1.0 / L);
     for (int j0 = h * 32; j0 < Nb; j0 += 64) {
       uint32_t rr[32];
       tc::ld_32x32b_x32(tmem + lane_base + 256 + j0, rr);
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       float pv[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        float v = row_ok ? ex2(__uint_as_float(rr[e]) - M) * inv_l : 0.f;
+        float v = row_ok ? exp2f((__uint_as_float(rr[e]) - M) * scale_log2) * inv_l : 0.f;
 #pragma unroll
         for (int o = 1; o < KK; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
         pv[e] = v;

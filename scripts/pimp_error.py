@@ -22,7 +22,7 @@ for wl, kw in (("wan", dict(tau=0.9, keep_min=51, keep_max=51)), ("wan", dict(ta
     print(wl, kw, "P_imp rel err: max %.3e  p99.9 %.3e  mean %.3e" % (rel.max(), np.quantile(rel, 0.999), rel.mean()))
     # margins of the oracle rows
     lo, hi = O.clamp_bounds(ref.p_imp.shape[1], O.AsaParams(**kw))
-    for guard in (1e-4, 3e-5, 1e-5, 3e-6):
+    for guard in (2e-5, 1e-5, 5e-6, 3e-6, 2e-6):
         mg = A.blade_asa_mask(qd, kd, refine_guard=guard, **kw)
         torch.cuda.synchronize()
         print("   guard %.0e -> rows refined %d of %d" % (guard, int(mg.n_refined.item()), BH * ref.p_imp.shape[1]))
