@@ -48,7 +48,7 @@ METRIC = "ASA fwd ms/call and effective TFLOPS (active blocks) vs bf16 peak at 1
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
     ap.add_argument("--workload", default="wan", choices=["wan", "cog", "tiny"])
@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--attn", default="auto", choices=["auto", "tcgen05", "mma"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gather", action="store_true",
+                    help="after timing, NCCL-gather every rank's O to rank 0 (BJ configs[4])")
     return ap.parse_args()
 
 
@@ -111,6 +113,12 @@ class ClockSampler:
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except (FileNotFoundError, OSError):
             self.p = None
+        t0 = time.time()  # wait for the first sample so the timed region is covered
+        while self.p is not None and time.time() - t0 < 3.0:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.02)
 
     def stop(self) -> dict:
         if self.p is None:
@@ -151,27 +159,32 @@ def traffic_for(workload: str, kernel: str):
 # ---------------------------------------------------------------------------
 
 
-def oracle_sample(q, k, v, w, mp, qblocks: int):
-    """Time the fp64 oracle on one unit: full mask, attention on `qblocks`
-    evenly spaced query blocks; returns (active FLOP of the whole unit,
-    estimated seconds for the whole unit, description)."""
+def oracle_sample(q, k, v, w, mp, units: int, qblocks: int | None):
+    """Time the fp64 oracle (as it stands) on `units` units: the full mask and
+    the attention of `qblocks` evenly spaced query blocks per unit (all if
+    None).  Returns (active FLOP of the sampled units' full calls, seconds
+    for those full calls, description); with a subset of query blocks the
+    attention seconds are scaled by active FLOP to the whole unit."""
     from oracle import asa_oracle as O
     p = O.AsaParams(tau=mp["tau"], keep_min=mp["keep_min"], keep_max=mp["keep_max"])
     t0 = time.perf_counter()
-    r = O.asa_mask(q[:1], k[:1], p)
+    r = O.asa_mask(q[:units], k[:units], p)
     t_mask = time.perf_counter() - t0
     Nb = r.kv_cnt.shape[1]
-    blocks = sorted(set(np.linspace(0, Nb - 1, qblocks).astype(int).tolist()))
+    blocks = (list(range(Nb)) if qblocks is None else
+              sorted(set(np.linspace(0, Nb - 1, qblocks).astype(int).tolist())))
     t0 = time.perf_counter()
-    O.sparse_attention(q[:1], k[:1], v[:1], r.kv_idx, r.kv_cnt, 128, qblocks=blocks)
+    O.sparse_attention(q[:units], k[:units], v[:units], r.kv_idx, r.kv_cnt, 128, qblocks=blocks)
     t_att = time.perf_counter() - t0
-    flop = active_flop(r.kv_idx, r.kv_cnt, w.N, w.d)
-    sample_flop = 4.0 * w.d * sum(min(128, w.N - i * 128) * sum(
-        min(128, w.N - j * 128) for j in r.kv_idx[0, i, :r.kv_cnt[0, i]]) for i in blocks)
-    est = t_mask + t_att * flop / max(sample_flop, 1.0)
-    desc = (f"1 of {w.B * w.H} units: full mask ({t_mask:.1f} s) + attention on {len(blocks)} of "
-            f"{Nb} query blocks ({t_att:.1f} s), scaled by active FLOP to the unit")
-    return flop, est, desc
+    valid = np.array([min(128, w.N - i * 128) for i in range(Nb)], dtype=np.float64)
+    f_blk = lambda u, i: 4.0 * w.d * valid[i] * valid[r.kv_idx[u, i, :r.kv_cnt[u, i]]].sum()
+    f_all = sum(f_blk(u, i) for u in range(units) for i in range(Nb))
+    f_smp = sum(f_blk(u, i) for u in range(units) for i in blocks)
+    secs = t_mask + t_att * f_all / f_smp
+    desc = (f"{units} of {w.B * w.H} units, fp64 numpy oracle: full mask ({t_mask:.2f} s) + "
+            f"attention of {len(blocks)} of {Nb} query blocks per unit ({t_att:.2f} s)"
+            + ("" if qblocks is None else ", attention time scaled by active FLOP to all blocks"))
+    return f_all, secs, desc
 
 
 def cores_used() -> int:
@@ -189,20 +202,17 @@ def run_reference(args, ws, rank):
     q, k, v = inputs.smooth(1, 1, w.N, w.d, w.grid, w.n_text, w.ell, w.beta, w.sigma_n, seed=42)
     Nb = (w.N + 127) // 128
     mp, mode = mask_params(w, args, Nb)
-    qb = 4 if args.workload != "tiny" else Nb
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm state worth discarding beyond the first sample
     vals, secs = [], []
     desc = ""
     for _ in range(args.steps):
-        flop, est, desc = oracle_sample(q, k, v, w, mp, qb)
-        vals.append(flop / est / 1e12)
-        secs.append(est)
+        flop, sec, desc = oracle_sample(q, k, v, w, mp, 1, 8 if args.workload != "tiny" else None)
+        vals.append(flop / sec / 1e12)
+        secs.append(sec)
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.median(secs) * 1e3 * w.B * w.H, "higher_is_better": True,
+        "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d, "mask": mode,
                    "tau": mp["tau"], "sample_per_step": desc},
@@ -282,16 +292,9 @@ def main():
     total_ms = t_begin.elapsed_time(t_end)
     attn_ms = statistics.mean(mids[s].elapsed_time(ends[s]) for s in range(args.steps))
     mask_ms = statistics.mean(starts[s].elapsed_time(mids[s]) for s in range(args.steps))
-    if ws > 1:
-        t = torch.tensor([total_ms, attn_ms, mask_ms, flop], device=dev, dtype=torch.float64)
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        total_ms, attn_ms, mask_ms = mx[0].item(), mx[1].item(), mx[2].item()
-        flop_all = sm[3].item()
-    else:
-        flop_all = flop
+    from paper_2508_10774_b200 import shard
+    total_ms, attn_ms, mask_ms = shard.max_over_ranks([total_ms, attn_ms, mask_ms], device=dev)
+    flop_all = shard.sum_over_ranks([flop], device=dev)[0]
     ms_per_step = total_ms / args.steps
     value = flop_all / (ms_per_step * 1e-3) / 1e12
 
@@ -323,11 +326,7 @@ def main():
             e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / args.steps
-        if ws > 1:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = t.item()
+        e2e_ms = shard.max_over_ranks([e0.elapsed_time(e1) / args.steps], device=dev)[0]
         e2e = {"value": flop_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * q_h.numel() * 2,
                "d2h_bytes_per_step": q_h.numel() * 2 + BH * N * 4}
@@ -343,12 +342,21 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        qb = 4 if args.workload != "tiny" else Nb
-        f1, est, desc = oracle_sample(q_h, k_h, v_h, w, mp, qb)
-        cpu = {"value": f1 / est / 1e12, "unit": "TFLOP/s", "cores": cores_used(),
+        f1, sec, desc = oracle_sample(q_h, k_h, v_h, w, mp, 2, None)
+        cpu = {"value": f1 / sec / 1e12, "unit": "TFLOP/s", "cores": cores_used(),
                "kind": "oracle", "sample": desc}
 
-    launches_per_step = 6 + (1 if mp.get("samples", 16) > 64 else 0)
+    gather = None
+    if args.gather and ws > 1:
+        o_local, _ = A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl)
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        o_all = shard.gather_units(o_local, ws * w.H)
+        torch.cuda.synchronize()
+        gather = {"bytes_to_rank0": (ws - 1) * o_local.numel() * 2,
+                  "seconds_wallclock": time.perf_counter() - g0,
+                  "shape": list(o_all.shape) if o_all is not None else None}
+    launches_per_step = 4  # sample_gather, probe(+select), refine, attention
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws,
@@ -366,6 +374,7 @@ def main():
             "ms_mask": mask_ms, "ms_attn": attn_ms,
             "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
+            "gather": gather,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int w = 32; w >= 1; w >>= 1)
 #pragma unroll
           for (int c = 0; c < w; ++c) s[c] += s[c + w];
-        if (m_new != m_run) l_run *= exp2((double(m_run) - double(m_new)) * double(scale_log2));
+        if (m_new != m_run) l_run *= double(ex2((m_run - m_new) * scale_log2));
         l_run += double(s[0]);
         m_run = m_new;
       }
@@ -206,9 +206,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     asm volatile("bar.sync 1, 256;\n" ::: "memory");
     const float m0 = smm[r], m1 = smm[128 + r];
     const float M = fmaxf(m0, m1);
-    const double sl2 = double(scale_log2);
-    const double L = (m0 == -INFINITY ? 0.0 : sml[r] * exp2((double(m0) - double(M)) * sl2)) +
-                     (m1 == -INFINITY ? 0.0 : sml[128 + r] * exp2((double(m1) - double(M)) * sl2));
+    const double L = (m0 == -INFINITY ? 0.0 : sml[r] * double(ex2((m0 - M) * scale_log2))) +
+                     (m1 == -INFINITY ? 0.0 : sml[128 + r] * double(ex2((m1 - M) * scale_log2)));
     // pooling (l.17-19): rows of query block i are KK consecutive lanes; the
     // two halves take alternate 32-column chunks of R
     const int gr = row0 + r;
@@ -222,7 +221,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       float pv[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        float v = row_ok ? exp2f((__uint_as_float(rr[e]) - M) * scale_log2) * inv_l : 0.f;
+        float v = row_ok ? ex2((__uint_as_float(rr[e]) - M) * scale_log2) * inv_l : 0.f;
 #pragma unroll
         for (int o = 1; o < KK; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
         pv[e] = v;
