@@ -27,6 +27,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+if os.environ.get("BLADE_EMU_MASK"):  # tuning experiments: attn exp-emulation pattern
+    FLAGS += [f"-DBLADE_ATTN_EMU_MASK={os.environ['BLADE_EMU_MASK']}"]
+    OBJDIR = os.path.join(ROOT, "build", "obj_emu" + os.environ["BLADE_EMU_MASK"])
+    LIB = os.path.join(LIBDIR, "libblade_asa_emu" + os.environ["BLADE_EMU_MASK"] + ".so")
 if os.environ.get("BLADE_DEBUG") == "1":  # hang watchdog + progress trace in attn_tc
     FLAGS += ["-DBLADE_TC_DEBUG"]
     OBJDIR = os.path.join(ROOT, "build", "obj_debug")

@@ -15,8 +15,10 @@
 // works on S(n); P(n) (bf16) overwrites the upper half of S(n)'s buffer and
 // feeds the P V MMA straight from TMEM.  MMA issue order:
 //   S(0) S(1) | PV(0) S(2) | PV(1) S(3) | ...
-// O is rescaled lazily (only when a row max grows by more than 2^8); a
-// quarter of the exponentials run as an FMA polynomial to unload MUFU.
+// The softmax is bound by the FMA and MUFU pipes, so the default softmax
+// scale is baked in (immediate-form FFMA), arithmetic is packed fp32x2, and some exponentials run
+// as an FMA-pipe polynomial (1 in 4 here) to balance the two.  O is rescaled lazily (only
+// when a row max grows by more than 2^8).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -50,6 +52,11 @@ struct Cfg {
 
 constexpr int kThreads = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P may reach 2^8 before O is rescaled
+// which of every 8 exponential PAIRS run on the FMA pipe (bit k: pair k)
+#ifndef BLADE_ATTN_EMU_MASK
+#define BLADE_ATTN_EMU_MASK 0x11  // pairs 0, 4: 2 of 8
+#endif
+constexpr uint32_t kEmuMask = BLADE_ATTN_EMU_MASK;
 
 #ifdef BLADE_TC_DEBUG
 #define TC_DBG(i, v)          \
@@ -62,27 +69,45 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units: P may reach 2^8 before
   } while (0)
 #endif
 
-// 2^x on the FMA pipe: x = n + f with n = rint(x) (1.5 * 2^23 trick), f in
-// [-1/2, 1/2], 2^f by its degree-4 Taylor polynomial (|rel err| < 5e-5, far
-// below the bf16 rounding P gets next), n added to the exponent field.
-BLADE_DEVINL float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 9.6181291e-3f, 5.5504109e-2f);
-  p = fmaf(p, f, 2.4022651e-1f);
-  p = fmaf(p, f, 6.9314718e-1f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// 2^x for a pair on the FMA pipe: x = n + f with n = rint(x) (1.5 * 2^23
+// trick), f in [-1/2, 1/2], 2^f by a degree-3 minimax polynomial (|rel err|
+// < 7.5e-5, far below the bf16 rounding P gets next), n added to the exponent
+// field.  Packed fp32x2 ops: 6 FMA-pipe slots for two exponentials.
+BLADE_DEVINL float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = add2(x, make_float2(12582912.f, 12582912.f));
+  const float2 n = add2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = fma2(f, make_float2(5.517165314e-2f, 5.517165314e-2f),
+                  make_float2(2.426111615e-1f, 2.426111615e-1f));
+  p = fma2(p, f, make_float2(6.932609919e-1f, 6.932609919e-1f));
+  p = fma2(p, f, make_float2(9.999280713e-1f, 9.999280713e-1f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// fp32(1/sqrt(d)) * fp32(log2 e) as the host computes it for the default
+// scale; baking it in lets the exponent FFMA use its immediate form.
 template <int D>
+struct DefaultScale;
+template <>
+struct DefaultScale<128> {
+  static constexpr float kScaleLog2 = 0.088388346f * 1.44269502f;
+};
+template <>
+struct DefaultScale<64> {
+  static constexpr float kScaleLog2 = 0.125f * 1.44269502f;
+};
+
+template <int D, bool kDefaultScale>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, int N, int Nb, float scale_log2,
+                   const __grid_constant__ CUtensorMap tmV, int N, int Nb, float scale_log2_rt,
                    const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
                    __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, volatile int* dbg) {
   using C = Cfg<D>;
+  const float scale_log2 = kDefaultScale ? DefaultScale<D>::kScaleLog2 : scale_log2_rt;
 #ifdef BLADE_TC_DEBUG
   const bool dbg_on = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
 #endif
@@ -261,23 +286,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         m_used = m_new;
       }
-      float acc0 = 0.f, acc1 = 0.f;
+      float2 acc = make_float2(0.f, 0.f);
+      const float2 sl2 = make_float2(scale_log2, scale_log2);
+      const float2 nm = make_float2(-m_used, -m_used);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const float x0 = fmaf(s[c * 32 + 2 * e], scale_log2, -m_used);
-          const float x1 = fmaf(s[c * 32 + 2 * e + 1], scale_log2, -m_used);
-          const float p0 = ex2(x0);
-          const float p1 = (e & 1) ? ex2_poly(x1) : ex2(x1);  // 1 in 4 on the FMA pipe
-          acc0 += p0;
-          acc1 += p1;
-          pk[e] = pack_bf16(p0, p1);
+          const float2 x = fma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sl2, nm);
+          float2 pp;
+          if ((kEmuMask >> (e & 7)) & 1) {
+            pp = ex2_poly2(x);
+          } else {
+            pp.x = ex2(x.x);
+            pp.y = ex2(x.y);
+          }
+          acc = add2(acc, pp);
+          pk[e] = pack_bf16(pp.x, pp.y);
         }
         tc::st_32x32b_x16(tS + 64 + c * 16, pk);
       }
-      l_sum += acc0 + acc1;
+      l_sum += acc.x + acc.y;
       tc::wait_st();
       tc::fence_before_sync();
       __syncwarp();
@@ -327,8 +357,9 @@ cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const v
       !make_tile_map(&mv, v, p.BH, p.N, D))
     return cudaErrorNotSupported;
   constexpr int smem = Cfg<D>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const bool dflt = p.scale == (D == 128 ? 0.088388346f : 0.125f);
+  auto kern = dflt ? attn_tc_kernel<D, true> : attn_tc_kernel<D, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(p.Nb), unsigned(p.BH));
   int* dbg_dev = nullptr;
@@ -340,7 +371,7 @@ cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const v
   memset(dbg_host, 0xff, 64 * sizeof(int));
   cudaHostGetDevicePointer(&dbg_dev, dbg_host, 0);
 #endif
-  attn_tc_kernel<D><<<grid, kThreads, smem, stream>>>(
+  kern<<<grid, kThreads, smem, stream>>>(
       mq, mk, mv, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
       reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev);
   e = cudaGetLastError();
