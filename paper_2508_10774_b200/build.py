@@ -31,6 +31,10 @@ if os.environ.get("BLADE_EMU_MASK"):  # tuning experiments: attn exp-emulation p
     FLAGS += [f"-DBLADE_ATTN_EMU_MASK={os.environ['BLADE_EMU_MASK']}"]
     OBJDIR = os.path.join(ROOT, "build", "obj_emu" + os.environ["BLADE_EMU_MASK"])
     LIB = os.path.join(LIBDIR, "libblade_asa_emu" + os.environ["BLADE_EMU_MASK"] + ".so")
+if os.environ.get("BLADE_EXP"):  # timing experiments: extra -D flags, separate lib name
+    FLAGS += [f"-D{x}" for x in os.environ["BLADE_EXP"].split(",")]
+    OBJDIR = os.path.join(ROOT, "build", "obj_" + os.environ["BLADE_EXP"].replace(",", "_"))
+    LIB = os.path.join(LIBDIR, "libblade_asa_" + os.environ["BLADE_EXP"].replace(",", "_") + ".so")
 if os.environ.get("BLADE_DEBUG") == "1":  # hang watchdog + progress trace in attn_tc
     FLAGS += ["-DBLADE_TC_DEBUG"]
     OBJDIR = os.path.join(ROOT, "build", "obj_debug")

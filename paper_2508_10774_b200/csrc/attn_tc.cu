@@ -7,10 +7,13 @@
 // lists of any length and order cost nothing extra.  Warp roles:
 //   warps 0-3  softmax (thread = query row = TMEM lane)
 //   warp  4    tcgen05.mma issuer (one thread) + TMEM allocator
-//   warp  5    TMA producer (one thread): Q once, then K_j / V_j slots of a
-//              smem ring in the order the MMA consumes them
-//   warps 6-7  idle (complete the second warpgroup)
-// TMEM (512 columns): S_0 [0,128) S_1 [128,256) O [256, 256+d).
+//   warp  5    TMA producer (one thread): Q once, then K_j into the K ring
+//   warp  6    TMA producer (one thread): V_j into the V ring
+//   warp  7    idle (completes the second warpgroup)
+// TMEM (512 columns): S_0 [0,128) S_1 [128,256) O [256, 256+d) Q [256+d, +d/2).
+// Q is copied into TMEM once, so S = Q K^T takes its A operand from TMEM and
+// the tensor core streams only K and V from shared memory (an SS MMA at
+// M = N = 128 would need the whole 128 B/clk of smem bandwidth by itself).
 // S is double-buffered, so S(n+1) = Q K(n+1)^T is computed while the softmax
 // works on S(n); P(n) (bf16) overwrites the upper half of S(n)'s buffer and
 // feeds the P V MMA straight from TMEM.  MMA issue order:
@@ -41,13 +44,26 @@ struct Cfg {
   static constexpr int kTile = 128 * D * 2;          // Q tile / K slot / V slot bytes
   static constexpr int kPanels = D / 64;             // 128-byte SW128 panels along d
   static constexpr int kPanel = 128 * 128;           // 128 rows x 128 B
-  static constexpr int kRing = D == 128 ? 5 : 10;    // K/V slots
-  static constexpr int kOffRing = kTile;
-  static constexpr int kOffBar = kOffRing + kRing * kTile;
-  static constexpr int kNumBar = 1 + 2 * kRing + 5;
+#ifndef BLADE_ATTN_KRING
+#define BLADE_ATTN_KRING 3
+#endif
+#ifndef BLADE_ATTN_VRING
+#define BLADE_ATTN_VRING 3
+#endif
+  // separate K and V rings: a K slot frees as soon as its S MMA completes,
+  // a V slot only after P V, so sharing one ring starves the K prefetch
+  static constexpr int kRingK = D == 128 ? BLADE_ATTN_KRING : 2 * BLADE_ATTN_KRING;
+  static constexpr int kRingV = D == 128 ? BLADE_ATTN_VRING : 2 * BLADE_ATTN_VRING;
+  static constexpr int kOffRingK = kTile;
+  static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
+  static constexpr int kOffBar = kOffRingV + kRingV * kTile;
+  // the Q tile's smem is free once Q sits in TMEM: it becomes one more V slot
+  static constexpr int kRingVx = kRingV + 1;
+  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingVx + 5 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
   static constexpr int kSmem = kOffMisc + 16 + 1024;  // + alignment slack
   static constexpr uint32_t kColO = 256;
+  static constexpr uint32_t kColQ = 256 + D;  // Q in TMEM (bf16 pairs): D / 2 columns
 };
 
 constexpr int kThreads = 256;
@@ -100,6 +116,22 @@ struct DefaultScale<64> {
   static constexpr float kScaleLog2 = 0.125f * 1.44269502f;
 };
 
+#ifdef BLADE_ATTN_TRACE  // timing experiment: event timeline of one CTA
+__device__ long long g_tr[8][64];
+#define TR(ev, n, cond)                                                               \
+  do {                                                                                \
+    if ((cond) && blockIdx.x == 100 && blockIdx.y == 5 && (n) < 64) g_tr[ev][n] = clock64(); \
+  } while (0)
+#else
+#define TR(ev, n, cond) \
+  do {                  \
+  } while (0)
+#endif
+#ifdef BLADE_ATTN_TIMING  // timing experiment: per-role cycle accounting
+__device__ unsigned long long g_tm[10];
+#define TM_ADD(i, v) atomicAdd(&g_tm[i], (unsigned long long)(v))
+#endif
+
 template <int D, bool kDefaultScale>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -114,17 +146,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   char* sQ = smem;
-  char* sRing = smem + C::kOffRing;
+  char* sRingK = smem + C::kOffRingK;
+  char* sRingV = smem + C::kOffRingV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* bar_q = bars;
-  uint64_t* bar_full = bars + 1;
-  uint64_t* bar_empty = bars + 1 + C::kRing;
-  uint64_t* bar_s = bars + 1 + 2 * C::kRing;   // [2] S buffer computed
+  uint64_t* bar_kfull = bars + 1;
+  uint64_t* bar_kempty = bar_kfull + C::kRingK;
+  uint64_t* bar_vfull = bar_kempty + C::kRingK;
+  uint64_t* bar_vempty = bar_vfull + C::kRingVx;
+  uint64_t* bar_s = bar_vempty + C::kRingVx;    // [2] S buffer computed
   uint64_t* bar_p = bar_s + 2;                  // [2] P written (4 warp arrivals)
   uint64_t* bar_pv = bar_p + 2;                 // one completion per P V MMA
+  uint64_t* bar_qt = bar_pv + 1;                // Q copied into TMEM (4 warp arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef BLADE_ATTN_TIMING
+  const long long t_cta0 = clock64();
+#endif
   const int i = blockIdx.x;
   const int64_t u = blockIdx.y;
   const int64_t row_id = u * Nb + i;
@@ -133,15 +172,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 5 && lane == 0) {
     tc::mbar_init(bar_q, 1);
-    for (int s = 0; s < C::kRing; ++s) {
-      tc::mbar_init(bar_full + s, 1);
-      tc::mbar_init(bar_empty + s, 1);
+    for (int s = 0; s < C::kRingK; ++s) {
+      tc::mbar_init(bar_kfull + s, 1);
+      tc::mbar_init(bar_kempty + s, 1);
+    }
+    for (int s = 0; s < C::kRingVx; ++s) {
+      tc::mbar_init(bar_vfull + s, 1);
+      tc::mbar_init(bar_vempty + s, 1);
     }
     tc::mbar_init(bar_s + 0, 1);
     tc::mbar_init(bar_s + 1, 1);
     tc::mbar_init(bar_p + 0, 4);
     tc::mbar_init(bar_p + 1, 4);
     tc::mbar_init(bar_pv, 1);
+    tc::mbar_init(bar_qt, 4);
     tc::fence_barrier_init();
   }
   if (warp == 4) tc::tmem_alloc<512>(tmem_slot);
@@ -150,32 +194,58 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5) {
-    // ===================== TMA producer =====================
-    // item order = MMA consumption order: K0 K1 | V0 K2 | V1 K3 | ... | V(cnt-1)
+  if (warp == 5 || warp == 6) {
+    // ===================== TMA producers (warp 5: Q and K, warp 6: V) ========
     if (lane == 0) {
-      tc::tma_prefetch_desc(&tmQ);
-      tc::tma_prefetch_desc(&tmK);
-      tc::tma_prefetch_desc(&tmV);
-      tc::mbar_arrive_expect_tx(bar_q, C::kTile);
-      for (int p = 0; p < C::kPanels; ++p)
-        tc::tma_load_3d(sQ + p * C::kPanel, &tmQ, bar_q, p * 64, i * 128, int(u));
-      uint32_t L = 0;
-      auto load = [&](const CUtensorMap* m, int j) {
-        const int s = L % C::kRing;
-        TC_DBG(0, int(L));
-        tc::mbar_wait(bar_empty + s, ((L / C::kRing) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(bar_full + s, C::kTile);
+      const bool isK = warp == 5;
+      if (isK) {
+        tc::tma_prefetch_desc(&tmQ);
+        tc::tma_prefetch_desc(&tmK);
+        tc::mbar_arrive_expect_tx(bar_q, C::kTile);
         for (int p = 0; p < C::kPanels; ++p)
-          tc::tma_load_3d(sRing + s * C::kTile + p * C::kPanel, m, bar_full + s, p * 64, j * 128,
-                          int(u));
-        ++L;
-      };
-      load(&tmK, list[0]);
-      if (cnt > 1) load(&tmK, list[1]);
+          tc::tma_load_3d(sQ + p * C::kPanel, &tmQ, bar_q, p * 64, i * 128, int(u));
+      } else {
+        tc::tma_prefetch_desc(&tmV);
+      }
+      const int R = isK ? C::kRingK : C::kRingVx;
+      char* ring = isK ? sRingK : sRingV;
+      uint64_t* full = isK ? bar_kfull : bar_vfull;
+      uint64_t* empty = isK ? bar_kempty : bar_vempty;
+      const CUtensorMap* m = isK ? &tmK : &tmV;
+#ifndef BLADE_ATTN_L2_PREFETCH
+#define BLADE_ATTN_L2_PREFETCH 0
+#endif
+      // warm L2 for the first blocks, then keep BLADE_ATTN_L2_PREFETCH blocks
+      // ahead of the ring: a block's first touch comes from HBM
+      for (int n = 0; n < BLADE_ATTN_L2_PREFETCH && n < cnt; ++n)
+        for (int p = 0; p < C::kPanels; ++p) tc::tma_prefetch_3d(m, p * 64, list[n] * 128, int(u));
       for (int n = 0; n < cnt; ++n) {
-        load(&tmV, list[n]);
-        if (n + 2 < cnt) load(&tmK, list[n + 2]);
+        const int s = n % R;
+        TC_DBG(0, n);
+        if (BLADE_ATTN_L2_PREFETCH > 0 && n + BLADE_ATTN_L2_PREFETCH < cnt)
+          for (int p = 0; p < C::kPanels; ++p)
+            tc::tma_prefetch_3d(m, p * 64, list[n + BLADE_ATTN_L2_PREFETCH] * 128, int(u));
+#ifdef BLADE_ATTN_TIMING
+        const long long te0 = clock64();
+#endif
+        tc::mbar_wait(empty + s, ((n / R) & 1) ^ 1);
+#ifdef BLADE_ATTN_TIMING
+        if (n >= R) TM_ADD(isK ? 8 : 9, clock64() - te0);
+#endif
+        TR(isK ? 0 : 1, n, true);
+#ifdef BLADE_ATTN_SKIP_KV_LOAD  // timing experiment only: MMA on stale smem
+        tc::mbar_arrive(full + s);
+#else
+        char* dst = ring + s * C::kTile;
+        if (!isK && s == C::kRingV) {  // the Q tile's slot: only after Q is in TMEM
+          if (n == C::kRingV) tc::mbar_wait(bar_qt, 0);
+          dst = sQ;
+        }
+        tc::mbar_arrive_expect_tx(full + s, C::kTile);
+        const int j = list[n];
+        for (int p = 0; p < C::kPanels; ++p)
+          tc::tma_load_3d(dst + p * C::kPanel, m, full + s, p * 64, j * 128, int(u));
+#endif
       }
     }
   } else if (warp == 4) {
@@ -183,47 +253,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
-      const uint32_t qa = smem_u32(sQ), rb = smem_u32(sRing);
-      uint32_t L = 0;
-      auto take = [&]() -> uint32_t {  // next ring item, waited for
-        const uint32_t s = L % C::kRing;
-        tc::mbar_wait(bar_full + s, (L / C::kRing) & 1);
+      const uint32_t kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
+      auto take = [&](uint64_t* full, int R, int n) -> uint32_t {  // slot of item n, waited for
+        const uint32_t s = n % R;
+#ifdef BLADE_ATTN_TIMING
+        const long long tf0 = clock64();
+#endif
+        tc::mbar_wait(full + s, (n / R) & 1);
+#ifdef BLADE_ATTN_TIMING
+        TM_ADD(n < 2 ? 7 : 4, clock64() - tf0);
+#endif
         tc::fence_after_sync();
-        ++L;
         return s;
       };
-      auto issue_S = [&](int buf) {
-        const uint32_t s = take();
-        const uint32_t kb = rb + s * C::kTile;
+      auto issue_S = [&](int n) {  // S(n) into buffer n & 1
+        const int buf = n & 1;
+        const uint32_t s = take(bar_kfull, C::kRingK, n);
+        TR(2, n, true);
+        const uint32_t kb = kbase + s * C::kTile;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-          tc::mma_ss(tmem + buf * 128, tc::sw128_desc(qa + off, 16, 1024),
-                     tc::sw128_desc(kb + off, 16, 1024), idS, ks > 0);
+          // A = Q from TMEM (16 d-values = 8 columns per k-step): the tensor core
+          // then reads only K from shared memory, which keeps the S MMA off the
+          // smem-bandwidth limit
+          tc::mma_ts(tmem + buf * 128, tmem + C::kColQ + ks * 8, tc::sw128_desc(kb + off, 16, 1024),
+                     idS, ks > 0);
         }
         tc::commit(bar_s + buf);
-        tc::commit(bar_empty + s);
+        tc::commit(bar_kempty + s);
       };
       TC_DBG(1, 1);
-      tc::mbar_wait(bar_q, 0);
+      tc::mbar_wait(bar_qt, 0);
       tc::fence_after_sync();
       issue_S(0);
       if (cnt > 1) issue_S(1);
       for (int n = 0; n < cnt; ++n) {
         const int buf = n & 1;
-        const uint32_t s = take();
+        const uint32_t s = take(bar_vfull, C::kRingVx, n);
+        TR(3, n, true);
         TC_DBG(1, 100 + n);
+#ifdef BLADE_ATTN_TIMING
+        const long long tp0 = clock64();
+#endif
         tc::mbar_wait(bar_p + buf, (n >> 1) & 1);
+#ifdef BLADE_ATTN_TIMING
+        TM_ADD(3, clock64() - tp0);
+#endif
         tc::fence_after_sync();
-        const uint32_t vb = rb + s * C::kTile;
+        TR(4, n, true);
+        const uint32_t vb = s < uint32_t(C::kRingV) ? vbase + s * C::kTile : smem_u32(sQ);
+#ifndef BLADE_ATTN_SKIP_PV  // timing experiment only
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
           tc::mma_ts(tmem + C::kColO, tmem + buf * 128 + 64 + ks * 8,
                      tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                      (n > 0 || ks > 0) ? 1 : 0);
+#endif
         tc::commit(bar_pv);
-        tc::commit(bar_empty + s);
-        if (n + 2 < cnt) issue_S(buf);
+        tc::commit(bar_vempty + s);
+        if (n + 2 < cnt) issue_S(n + 2);
       }
       // drain: the last commits must land before the CTA's smem is released
       tc::mbar_wait(bar_pv, (cnt - 1) & 1);
@@ -233,13 +322,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== softmax =====================
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
     const uint32_t tO = tmem + lane_base + C::kColO;
+    {  // Q row (this thread's) from the swizzled smem tile into TMEM columns
+      const int r = warp * 32 + lane;
+      tc::mbar_wait(bar_q, 0);
+#pragma unroll
+      for (int p = 0; p < C::kPanels; ++p) {
+        uint32_t q32[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sQ + p * C::kPanel + r * 128 +
+                                                          ((c ^ (r & 7)) << 4));
+          q32[4 * c + 0] = v.x;
+          q32[4 * c + 1] = v.y;
+          q32[4 * c + 2] = v.z;
+          q32[4 * c + 3] = v.w;
+        }
+        tc::st_32x32b_x32(tmem + lane_base + C::kColQ + p * 32, q32);
+      }
+      tc::wait_st();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bar_qt);
+    }
     float m_used = -INFINITY, l_sum = 0.f;
     for (int n = 0; n < cnt; ++n) {
       const int buf = n & 1;
       const uint32_t tS = tmem + lane_base + buf * 128;
       if (lane == 0) TC_DBG(2 + warp, 10 * n + 1);
+#ifdef BLADE_ATTN_TIMING
+      const long long tw0 = clock64();
+#endif
       tc::mbar_wait(bar_s + buf, (n >> 1) & 1);
       tc::fence_after_sync();
+      TR(5, n, warp == 0 && lane == 0);
+#ifdef BLADE_ATTN_TIMING
+      const long long tw1 = clock64();
+#endif
+#ifdef BLADE_ATTN_SKIP_SOFTMAX  // timing experiment only: MMA/TMA pipeline alone
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bar_p + buf);
+      continue;
+#endif
       float s[128];
       {
         uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -262,9 +386,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 128; ++c)
           if (c >= valid) s[c] = -INFINITY;
       }
-      float mx = fmaxf(s[0], s[1]);
+      // row max as a tree (a linear chain would serialise 64 ALU latencies)
+      float mx;
+      {
+        float t8[8];
 #pragma unroll
-      for (int c = 2; c < 128; c += 2) mx = fmaxf(mx, fmaxf(s[c], s[c + 1]));
+        for (int g = 0; g < 8; ++g) {
+          float a = fmaxf(s[g], s[g + 8]);
+#pragma unroll
+          for (int c = g + 16; c < 128; c += 16) a = fmaxf(a, fmaxf(s[c], s[c + 8]));
+          t8[g] = a;
+        }
+        mx = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
+                   fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
+      }
       const float mxs = mx * scale_log2;
       // warp-uniform (tcgen05.ld/st are .sync.aligned); always true for n = 0
       if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
@@ -286,7 +421,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         m_used = m_new;
       }
-      float2 acc = make_float2(0.f, 0.f);
+      float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};  // independent partial sums (ILP)
       const float2 sl2 = make_float2(scale_log2, scale_log2);
       const float2 nm = make_float2(-m_used, -m_used);
 #pragma unroll
@@ -302,16 +438,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             pp.x = ex2(x.x);
             pp.y = ex2(x.y);
           }
-          acc = add2(acc, pp);
+          acc4[e & 3] = add2(acc4[e & 3], pp);
           pk[e] = pack_bf16(pp.x, pp.y);
         }
         tc::st_32x32b_x16(tS + 64 + c * 16, pk);
       }
+      const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
       l_sum += acc.x + acc.y;
       tc::wait_st();
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bar_p + buf);
+      TR(6, n, warp == 0 && lane == 0);
+#ifdef BLADE_ATTN_TIMING
+      if (lane == 0) {
+        const long long tw2 = clock64();
+        TM_ADD(0, tw1 - tw0);
+        TM_ADD(1, tw2 - tw1);
+        TM_ADD(2, 1);
+      }
+#endif
     }
     // epilogue: O / l -> bf16, LSE
     if (lane == 0) TC_DBG(2 + warp, 9000);
@@ -346,6 +492,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tmem_dealloc<512>(tmem);
   }
   if (tid == 0) TC_DBG(11, 777);
+#ifdef BLADE_ATTN_TIMING
+  if (tid == 0) {
+    TM_ADD(5, clock64() - t_cta0);
+    TM_ADD(6, 1);
+  }
+#endif
 }
 
 template <int D>
@@ -375,6 +527,39 @@ cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const v
       mq, mk, mv, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
       reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev);
   e = cudaGetLastError();
+#ifdef BLADE_ATTN_TRACE
+  {
+    static int calls = 0;
+    long long h[8][64];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    if (++calls == 10) {
+      const long long t0 = h[0][0];
+      fprintf(stderr, "n: Kissue Vissue Ktake Vtake Pready(MMA) SMstart SMdone (cycles from first K issue)\n");
+      for (int n = 0; n < 24; ++n)
+        fprintf(stderr, "%2d: %7lld %7lld %7lld %7lld %7lld %7lld %7lld\n", n, h[0][n] - t0,
+                h[1][n] - t0, h[2][n] - t0, h[3][n] - t0, h[4][n] - t0, h[5][n] - t0, h[6][n] - t0);
+    }
+  }
+#endif
+#ifdef BLADE_ATTN_TIMING
+  {
+    static int calls = 0;
+    unsigned long long z[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, h[10];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h, g_tm, sizeof(h));
+    cudaMemcpyToSymbol(g_tm, z, sizeof(z));
+    if (++calls % 20 == 0 && h[2] && h[6])
+      fprintf(stderr,
+              "attn timing: softmax wait-S %.0f, compute %.0f cyc/tile/warp; MMA wait-P %.0f, "
+              "wait-data %.0f cyc/item (first two items of a CTA: %.0f cyc per CTA); CTA %.0f "
+              "cyc, %.1f tiles/CTA; loader wait-empty K %.0f V %.0f cyc/item\n",
+              double(h[0]) / h[2], double(h[1]) / h[2], double(h[3]) / (h[2] / 4.0),
+              double(h[4]) / (h[2] / 2.0 - 4.0 * h[6]), double(h[7]) / h[6],
+              double(h[5]) / h[6], h[2] / 4.0 / h[6], double(h[8]) / (h[2] / 4.0),
+              double(h[9]) / (h[2] / 4.0));
+  }
+#endif
 #ifdef BLADE_TC_DEBUG
   if (e == cudaSuccess) {
     for (int it = 0; it < 500 && cudaStreamQuery(stream) == cudaErrorNotReady; ++it) usleep(10000);

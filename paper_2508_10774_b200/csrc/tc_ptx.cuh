@@ -56,6 +56,14 @@ BLADE_DEVINL void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, in
       : "memory");
 }
 
+// L2 prefetch of a 3-D tile (no smem destination, no barrier)
+BLADE_DEVINL void tma_prefetch_3d(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 // ---- tcgen05 ----------------------------------------------------------------
 template <uint32_t kCols>
 BLADE_DEVINL void tmem_alloc(uint32_t* dst_smem) {  // whole warp
