@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <float.h>
 #include <math.h>
+#include <stdio.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -344,16 +345,21 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(
 // P_imp row (l.17-19) and reselects it.  The reselection sorts the fp64
 // values rounded to fp32 (relative error 6e-8, far inside the 1e-6 tie band).
 // ---------------------------------------------------------------------------
-constexpr int RF_KEYS = 128;
+constexpr int RF_THREADS = 128;
 
-template <int D>
-__global__ void __launch_bounds__(RF_KEYS, 3) refine_kernel(
+// CK = sampled keys per work item (64 for k <= 64, 128 for k = 128): a thread
+// owns one key and RPT = 16 CK / 128 of the block's (up to 16) query rows.
+template <int D, int CK>
+__global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N, int Nb,
     int b, int kk, double scale, int nchunks, double tau, int lo, int hi,
     const int* __restrict__ counters, const int32_t* __restrict__ flags, int* __restrict__ done,
     double* __restrict__ r64, double* __restrict__ mpart, double* __restrict__ lpart,
     float* __restrict__ pimp_out, uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx,
     int32_t* __restrict__ kv_cnt, int32_t* __restrict__ n_refined) {
+  constexpr int RPT = 16 * CK / RF_THREADS;  // query rows per thread
+  constexpr int NG = CK / 16;                // 16-key groups per item
+  constexpr int WPH = CK / 32;               // warps per row-half
   __shared__ __align__(16) double sq[D][16];   // [d][s]: one LDS.128 serves two query rows
   __shared__ double sRg[8][16];                // [16-key group][s] group max
   __shared__ double sW[4][16];                 // per-warp partials
@@ -363,6 +369,7 @@ __global__ void __launch_bounds__(RF_KEYS, 3) refine_kernel(
   __shared__ uint32_t keep_bits[16];
   __shared__ int last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kt = tid % CK, hr = tid / CK;
   const int nflag = counters[0];
   if (blockIdx.x == 0 && tid == 0 && n_refined) *n_refined = nflag;
   const int NK = Nb * kk;
@@ -372,49 +379,56 @@ __global__ void __launch_bounds__(RF_KEYS, 3) refine_kernel(
     const int64_t u = row / Nb;
     const int i = int(row % Nb);
     const int ki = min(kk, min(b, N - i * b));
-    const int key = c * RF_KEYS + tid;
+    const int key = c * CK + kt;
     const int jb = key / kk, rr = key - jb * kk;
     const bool kvalid = key < NK && rr < min(kk, min(b, N - jb * b));
     const __nv_bfloat16* kp = ks + (u * NK + min(key, NK - 1)) * int64_t(D);
     for (int sg = 0; sg < kk; sg += 16) {
       __syncthreads();
-      for (int e = tid; e < 16 * D; e += RF_KEYS) {
-        const int sq_s = e & 15, dd = e >> 4;
-        sq[dd][sq_s] =
-            double(__bfloat162float(qs[(u * NK + int64_t(i) * kk + sg + sq_s) * D + dd]));
+      // coalesced: thread t reads 8 consecutive bf16 of query row t / (D/8)
+      for (int e = tid; e < 16 * (D / 8); e += RF_THREADS) {
+        const int sq_s = e / (D / 8), d8 = (e % (D / 8)) * 8;
+        const uint4 raw = *reinterpret_cast<const uint4*>(
+            qs + (u * NK + int64_t(i) * kk + sg + sq_s) * D + d8);
+        const __nv_bfloat16* hq = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) sq[d8 + z][sq_s] = double(__bfloat162float(hq[z]));
       }
       __syncthreads();
-      double L[16];
+      double L[RPT];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) L[q] = 0.0;
-#pragma unroll 1
+      for (int q = 0; q < RPT; ++q) L[q] = 0.0;
+      uint4 krow[D / 8];  // the whole key row up front: one memory latency, not D/8
+#pragma unroll
+      for (int d0 = 0; d0 < D; d0 += 8) krow[d0 / 8] = *reinterpret_cast<const uint4*>(kp + d0);
+#pragma unroll
       for (int d0 = 0; d0 < D; d0 += 8) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(kp + d0);
+        const uint4 raw = krow[d0 / 8];
         const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const double kv = double(__bfloat162float(h[e]));
 #pragma unroll
-          for (int q = 0; q < 16; q += 2) {
-            const double2 qq = *reinterpret_cast<const double2*>(&sq[d0 + e][q]);
+          for (int q = 0; q < RPT; q += 2) {
+            const double2 qq = *reinterpret_cast<const double2*>(&sq[d0 + e][hr * RPT + q]);
             L[q] = fma(qq.x, kv, L[q]);
             L[q + 1] = fma(qq.y, kv, L[q + 1]);
           }
         }
       }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) L[q] = kvalid ? L[q] * scale : -INFINITY;
-      // per 16-key group max (a key block when kk = 16)
+      for (int q = 0; q < RPT; ++q) L[q] = kvalid ? L[q] * scale : -INFINITY;
+      // per 16-key group max (a key block when kk = 16); 16 consecutive lanes
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < RPT; ++q) {
         double v = L[q];
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if ((lane & 15) == 0) sRg[tid >> 4][q] = v;
+        if ((lane & 15) == 0) sRg[kt >> 4][hr * RPT + q] = v;
       }
       __syncthreads();
-      const int gpb = kk / 16;          // 16-key groups per key block
-      const int nblk = RF_KEYS / kk;    // key blocks per chunk (kk <= 128)
+      const int gpb = kk / 16;     // 16-key groups per key block
+      const int nblk = CK / kk;    // key blocks per item (kk <= CK)
       if (tid < 16 * nblk) {
         const int q = tid & 15, bl = tid >> 4;
         double v = -INFINITY;
@@ -424,20 +438,25 @@ __global__ void __launch_bounds__(RF_KEYS, 3) refine_kernel(
       }
       if (tid < 16) {
         double v = -INFINITY;
-        for (int gg = 0; gg < 8; ++gg) v = fmax(v, sRg[gg][tid]);
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) v = fmax(v, sRg[gg][tid]);
         sMc[tid] = v;
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        double e = (L[q] == -INFINITY) ? 0.0 : exp(L[q] - sMc[q]);
+      for (int q = 0; q < RPT; ++q) {
+        const double mc = sMc[hr * RPT + q];
+        double e = (L[q] == -INFINITY) ? 0.0 : exp(L[q] - mc);
 #pragma unroll
         for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
         if (lane == 0) sW[warp][q] = e;
       }
       __syncthreads();
       if (tid < 16 && sg + tid < ki) {
-        const double l = sW[0][tid] + sW[1][tid] + sW[2][tid] + sW[3][tid];
+        const int h2 = tid / RPT, q = tid % RPT;  // the row-half that owns query row tid
+        double l = 0.0;
+#pragma unroll
+        for (int w = 0; w < WPH; ++w) l += sW[h2 * WPH + w][q];
         const int64_t o = (int64_t(f) * nchunks + c) * kk + sg + tid;
         mpart[o] = sMc[tid];
         lpart[o] = l;
@@ -450,24 +469,42 @@ __global__ void __launch_bounds__(RF_KEYS, 3) refine_kernel(
     __syncthreads();
     if (!last) continue;
     __threadfence();
-    if (tid < ki) {
+    // l.14 combine, spread over all threads: (query row q, chunk stripe z)
+    {
+      const int q = tid & 15, z = tid >> 4;  // 16 rows x 8 stripes
       double M = -INFINITY;
-      for (int cc = 0; cc < nchunks; ++cc)
-        M = fmax(M, __ldcg(&mpart[(int64_t(f) * nchunks + cc) * kk + tid]));
+      if (q < ki)
+        for (int cc = z; cc < nchunks; cc += 8)
+          M = fmax(M, __ldcg(&mpart[(int64_t(f) * nchunks + cc) * kk + q]));
+      sRg[z][q] = M;
+      __syncthreads();
+      M = sRg[0][q];
+#pragma unroll
+      for (int zz = 1; zz < 8; ++zz) M = fmax(M, sRg[zz][q]);
       double l = 0.0;
-      for (int cc = 0; cc < nchunks; ++cc) {
-        const int64_t o = (int64_t(f) * nchunks + cc) * kk + tid;
-        const double mc = __ldcg(&mpart[o]);
-        if (mc != -INFINITY) l += __ldcg(&lpart[o]) * exp(mc - M);
+      if (q < ki)
+        for (int cc = z; cc < nchunks; cc += 8) {
+          const int64_t o = (int64_t(f) * nchunks + cc) * kk + q;
+          const double mc = __ldcg(&mpart[o]);
+          if (mc != -INFINITY) l += __ldcg(&lpart[o]) * exp(mc - M);
+        }
+      __syncthreads();
+      sRg[z][q] = l;
+      __syncthreads();
+      if (z == 0 && q < ki) {
+        double lt = 0.0;
+#pragma unroll
+        for (int zz = 0; zz < 8; ++zz) lt += sRg[zz][q];
+        sMs[q] = M + log(lt);  // P~ = e^{L - M} / l = e^{L - (M + ln l)}
       }
-      sMs[tid] = M;
-      sLs[tid] = 1.0 / l;
     }
     __syncthreads();
-    for (int j = tid; j < Nb; j += RF_KEYS) {
-      double best = 0.0;
+    // l.17-19: P_imp[j] = max_s e^{R_sj - M_s} / l_s = e^{max_s (R_sj - M_s - ln l_s)}
+    for (int j = tid; j < Nb; j += RF_THREADS) {
+      double arg = -INFINITY;
       for (int q = 0; q < ki; ++q)
-        best = fmax(best, exp(__ldcg(&r64[(int64_t(f) * kk + q) * Nb + j]) - sMs[q]) * sLs[q]);
+        arg = fmax(arg, __ldcg(&r64[(int64_t(f) * kk + q) * Nb + j]) - sMs[q]);
+      const double best = exp(arg);
       sRow[j] = float(best);
       if (pimp_out) pimp_out[row * Nb + j] = float(best);
     }
@@ -528,9 +565,14 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         kv_cnt, counters, flags, done);
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
-  refine_kernel<D><<<148 * 8, RF_KEYS, 0, stream>>>(
-      qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
-      flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
+  if (p.kk <= 64)
+    refine_kernel<D, 64><<<148 * 3, RF_THREADS, 0, stream>>>(
+        qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
+        flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
+  else
+    refine_kernel<D, 128><<<148 * 3, RF_THREADS, 0, stream>>>(
+        qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
+        flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
   return cudaGetLastError();
 }
 
