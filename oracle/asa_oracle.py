@@ -464,3 +464,102 @@ def check_row_against(sel: RowSelection, tau: float, lo: int, hi: int,
         if j not in kept and pj > (1 + eps) * pivot:
             return f"dropped block {j} p={pj} above pivot {pivot}"
     return None
+
+
+# ---------------------------------------------------------------------------
+# F1  ASA with global tokens, ASA_GT (P:135 Step 2.2 (2); Fig. 2
+#     caption): K_aug = Concat(K, MeanPool_n(K)), V_aug likewise; the
+#     original region keeps the binary block mask M, the pooled region
+#     ("global tokens") is attended by every query with a fixed additive
+#     pre-softmax bias ln(n).  Readings:
+#       R-18  windows are consecutive runs of n tokens [w n, min((w+1) n, N));
+#             N_g = ceil(N / n); a partial last window is the mean of its
+#             n_w < n real tokens and carries bias ln(n_w) (= ln n for every
+#             full window, "as if it represents the full importance of
+#             its n constituent fine-grained tokens").
+#       R-19  K_aug / V_aug are tensors of the input dtype (Concat needs one
+#             dtype), so the pooled rows are the exact means rounded once to
+#             bf16 (round-to-nearest-even).
+#       R-20  the mask M (Alg. 1) is computed from Q and K only, unchanged;
+#             global tokens join the same softmax, so LSE includes them.
+# ---------------------------------------------------------------------------
+
+
+def round_to_bf16(x: np.ndarray) -> np.ndarray:
+    """Round fp64 values to the nearest bf16 value (8 significant bits, ties
+    to even), returned as fp64.  One rounding step (no fp32 detour); bf16
+    normal range only (|x| >= 2^-126 or 0), which the pooled means of bf16
+    inputs of realistic size never leave."""
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)                 # x = m 2^e, 0.5 <= |m| < 1
+    r = np.round(m * 256.0)            # 8 significant bits; numpy rounds half to even
+    return np.ldexp(r, e - 8)
+
+
+def mean_pool_windows(x_u: np.ndarray, n: int):
+    """MeanPool_n over the token axis (reading R-18): returns the
+    pooled rows [N_g, d] (exact fp64 means, NOT yet rounded) and the window
+    sizes n_w [N_g]."""
+    x_u = to_f64(x_u)
+    N = x_u.shape[0]
+    Ng = (N + n - 1) // n
+    pooled = np.empty((Ng, x_u.shape[1]))
+    counts = np.empty(Ng, dtype=np.int64)
+    for w in range(Ng):
+        rows = x_u[w * n:min((w + 1) * n, N)]
+        counts[w] = rows.shape[0]
+        pooled[w] = rows.sum(axis=0) / rows.shape[0]
+    return pooled, counts
+
+
+def global_tokens(k_u, v_u, n: int):
+    """The ASA_GT global tokens of one unit: (K_g, V_g, bias) with K_g, V_g
+    the bf16-rounded window means (R-19) and bias_w = ln(n_w) (R-18)."""
+    kg, counts = mean_pool_windows(k_u, n)
+    vg, _ = mean_pool_windows(v_u, n)
+    return round_to_bf16(kg), round_to_bf16(vg), np.log(counts.astype(np.float64))
+
+
+def sparse_attention_gt_unit(q_u, k_u, v_u, kv_idx_u, kv_cnt_u, b: int, scale: float,
+                             n: int, qblocks=None):
+    """ASA_GT attention of one unit, fp64.  For query row r of q-block i:
+        T     = union over kept j of [j*b, min((j+1)*b, N))     (mask M)
+        s_t   = scale * q_r . k_t                 for t in T
+        g_w   = scale * q_r . K_g[w] + ln(n_w)    for every window w
+        LSE_r = ln( sum_{t in T} e^{s_t} + sum_w e^{g_w} )
+        O_r   = sum_{t in T} e^{s_t - LSE_r} v_t + sum_w e^{g_w - LSE_r} V_g[w]
+    Returns (O [N, d], LSE [N]); rows of q-blocks not in ``qblocks`` are NaN."""
+    q_u, k_u, v_u = to_f64(q_u), to_f64(k_u), to_f64(v_u)
+    N, d = q_u.shape
+    Nb = num_blocks(N, b)
+    kg, vg, bias = global_tokens(k_u, v_u, n)
+    O = np.full((N, v_u.shape[1]), np.nan)
+    LSE = np.full(N, np.nan)
+    for i in (range(Nb) if qblocks is None else qblocks):
+        r0, r1 = i * b, min((i + 1) * b, N)
+        cols = np.concatenate([np.arange(j * b, min((j + 1) * b, N))
+                               for j in kv_idx_u[i, :kv_cnt_u[i]]])
+        S = (q_u[r0:r1] @ k_u[cols].T) * scale
+        G = (q_u[r0:r1] @ kg.T) * scale + bias[None, :]
+        A = np.concatenate([S, G], axis=1)
+        Vaug = np.concatenate([v_u[cols], vg], axis=0)
+        mx = A.max(axis=1, keepdims=True)
+        E = np.exp(A - mx)
+        ell = E.sum(axis=1, keepdims=True)
+        O[r0:r1] = (E @ Vaug) / ell
+        LSE[r0:r1] = (mx + np.log(ell))[:, 0]
+    return O, LSE
+
+
+def sparse_attention_gt(q, k, v, kv_idx, kv_cnt, b: int, n: int, scale: float | None = None,
+                        units=None, qblocks=None):
+    """ASA_GT attention for [BH, N, d] inputs; fp64 O [BH, N, d], LSE [BH, N]."""
+    q, k, v = to_f64(q), to_f64(k), to_f64(v)
+    BH, N, d = q.shape
+    scale = default_scale(d) if scale is None else float(scale)
+    O = np.full(q.shape[:2] + (v.shape[2],), np.nan)
+    LSE = np.full((BH, N), np.nan)
+    for u in (range(BH) if units is None else units):
+        O[u], LSE[u] = sparse_attention_gt_unit(q[u], k[u], v[u], kv_idx[u], kv_cnt[u], b,
+                                                scale, n, qblocks)
+    return O, LSE
