@@ -51,13 +51,19 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
-    ap.add_argument("--workload", default="wan", choices=["wan", "cog", "tiny"])
+    ap.add_argument("--workload", default="wan", choices=["wan", "cog", "tiny", "wan_stack"])
+    ap.add_argument("--layers", type=int, default=30, help="wan_stack: attention layers per step")
     ap.add_argument("--keep", type=int, default=None,
                     help="keep-ratio mode: lo = hi = KEEP blocks per row (default 51 wan / 25 cog)")
     ap.add_argument("--tau-mode", action="store_true", help="pure tau mode (lo=ceil(.05 Nb), hi=Nb)")
     ap.add_argument("--tau", type=float, default=0.9)
     ap.add_argument("--attn", default="auto", choices=["auto", "tcgen05", "mma"])
+    ap.add_argument("--variant", default="asa", choices=["asa", "asa_gt"],
+                    help="asa_gt: ASA with global tokens (P:135), MeanPool window --window")
+    ap.add_argument("--window", type=int, default=128)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="units per chunk of the host-buffer pipeline (0 = library default)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true",
                     help="after timing, NCCL-gather every rank's O to rank 0 (BJ configs[4])")
@@ -74,7 +80,8 @@ def dist_env():
 def mask_params(w, args, Nb):
     if args.tau_mode:
         return dict(tau=args.tau, keep_min=max(1, -(-5 * Nb // 100)), keep_max=Nb), "tau"
-    keep = args.keep if args.keep is not None else {"wan": 51, "cog": 25, "tiny": 2}[args.workload]
+    keep = args.keep if args.keep is not None else {"wan": 51, "cog": 25, "tiny": 2,
+                                                    "wan_stack": 51}[args.workload]
     keep = min(keep, Nb)
     return dict(tau=args.tau, keep_min=keep, keep_max=keep), f"keep{keep}"
 
@@ -229,11 +236,86 @@ def run_reference(args, ws, rank):
 # ---------------------------------------------------------------------------
 
 
+def run_stack(args, ws, rank, local, dev):
+    """BASELINE.json configs[4]: the Wan2.1-1.3B attention stack, batch 8 x
+    30 layers, (batch, head) units sharded over the ranks (strong scaling:
+    the total work is fixed), per-layer inputs generated on the device
+    before timing, and the last layer's O gathered to rank 0 over NCCL
+    inside the timed step."""
+    from paper_2508_10774_b200 import asa as A
+    from paper_2508_10774_b200 import shard
+    w = inputs.WORKLOADS["wan_stack"]
+    units = w.B * w.H
+    lo, hi = shard.unit_range(ws, rank, units)
+    Nb = (w.N + 127) // 128
+    mp, mode = mask_params(w, args, Nb)
+    layers = []
+    for layer in range(args.layers):  # seed 42 + layer; each rank draws only its units
+        q, k, v = inputs.smooth_device(hi - lo, w.N, w.d, w.grid, dev, ell=w.ell, beta=w.beta,
+                                       sigma_n=w.sigma_n, seed=(42 + layer) * 1000 + lo)
+        layers.append((q, k, v))
+    stream = torch.cuda.current_stream()
+    o_last = torch.empty_like(layers[0][0])
+
+    def step(gather: bool):
+        m = None
+        for li, (q, k, v) in enumerate(layers):
+            m = A.blade_asa_mask(q, k, unit_offset=lo, want_mask=False, seed=42 + li, **mp)
+            A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, o=o_last if li == len(layers) - 1
+                            else None, want_lse=False)
+        if gather and ws > 1:
+            shard.gather_units(o_last, units)
+        return m
+
+    flop = 0.0
+    for li, (q, k, v) in enumerate(layers):  # active FLOP of this rank's units, every layer
+        m = A.blade_asa_mask(q, k, unit_offset=lo, want_mask=False, seed=42 + li, **mp)
+        flop += active_flop(m.kv_idx.cpu().numpy(), m.kv_cnt.cpu().numpy(), w.N, w.d)
+    for _ in range(max(args.warmup, 3)):
+        step(True)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = shard.max_over_ranks([e0.elapsed_time(e1) / args.steps], device=dev)[0]
+    flop_all = shard.sum_over_ranks([flop], device=dev)[0]
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": flop_all / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (smooth-field Q/K drawn on device, iid V; DESIGN.md §Inputs)",
+            "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d,
+                       "layers": args.layers, "mask": mode, "units_per_rank": hi - lo,
+                       "parallelism": f"(batch,head)-sharded x{ws}; NCCL gather of the last "
+                       "layer's O to rank 0 inside the step",
+                       "l2": "inputs larger than L2, no flush"},
+            "ms_per_layer": ms / args.layers, "clocks": clocks,
+            "gpu_launches": 4 * args.layers * args.steps}), flush=True)
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if args.workload == "wan_stack":
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=dev)
+        run_stack(args, ws, rank, local, dev)
+        if ws > 1:
+            torch.distributed.destroy_process_group()
         return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -254,10 +336,18 @@ def main():
     stream = torch.cuda.current_stream()
     unit_offset = rank * w.H
 
+    gt = args.variant == "asa_gt"
+
     def step():
+        if gt:  # ASA_GT: MeanPool_n counts as mask-side work
+            kg, vg = A.blade_gt_pool(k, v, window=args.window)
         m = A.blade_asa_mask(q, k, unit_offset=unit_offset, want_mask=False, **mp)
         ev_mid.record(stream)
-        A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl)
+        if gt:
+            A.blade_bsa_gt_fwd(q, k, v, m.kv_idx, m.kv_cnt, kg, vg, window=args.window,
+                               impl=impl)
+        else:
+            A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl)
         return m
 
     ev_mid = torch.cuda.Event(enable_timing=True)
@@ -266,6 +356,8 @@ def main():
     torch.cuda.synchronize()
     kv_idx_np, kv_cnt_np = m.kv_idx.cpu().numpy(), m.kv_cnt.cpu().numpy()
     flop = active_flop(kv_idx_np, kv_cnt_np, N, d)
+    if gt:  # every query row also attends the N_g global tokens
+        flop += 4.0 * d * BH * N * A.num_global_tokens(N, args.window)
     refined = int(m.n_refined.item())
     sparsity = 1.0 - kv_cnt_np.sum() / (BH * Nb * Nb)
 
@@ -300,20 +392,15 @@ def main():
 
     # e2e: host buffers through the ABI, copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not gt:  # the host-buffer entry point runs plain ASA
         qp, kp, vp = (t.pin_memory() for t in (q_h, k_h, v_h))
         o_host = torch.empty_like(q_h).pin_memory()
         lse_host = torch.empty((BH, N), dtype=torch.float32).pin_memory()
-        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
 
         def e2e_step():
-            qd.copy_(qp, non_blocking=True)
-            kd.copy_(kp, non_blocking=True)
-            vd.copy_(vp, non_blocking=True)
-            mm = A.blade_asa_mask(qd, kd, unit_offset=unit_offset, want_mask=False, **mp)
-            o, lse = A.blade_bsa_fwd(qd, kd, vd, mm.kv_idx, mm.kv_cnt, impl=impl)
-            o_host.copy_(o, non_blocking=True)
-            lse_host.copy_(lse, non_blocking=True)
+            # the public host-buffer entry point: chunked H2D / compute / D2H overlap
+            A.blade_asa_fwd_host(qp, kp, vp, unit_offset=unit_offset, impl=impl,
+                                 chunk_units=args.e2e_chunk, o=o_host, lse=lse_host, **mp)
 
         for _ in range(2):
             e2e_step()
@@ -328,7 +415,8 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = shard.max_over_ranks([e0.elapsed_time(e1) / args.steps], device=dev)[0]
         e2e = {"value": flop_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * q_h.numel() * 2,
+               "ms_per_step": e2e_ms, "api": "blade_asa_fwd_host (C ABI, pinned host buffers, "
+               "chunked copy/compute overlap)", "h2d_bytes_per_step": 3 * q_h.numel() * 2,
                "d2h_bytes_per_step": q_h.numel() * 2 + BH * N * 4}
 
     pk, pk_src = peaks()
@@ -356,7 +444,7 @@ def main():
         gather = {"bytes_to_rank0": (ws - 1) * o_local.numel() * 2,
                   "seconds_wallclock": time.perf_counter() - g0,
                   "shape": list(o_all.shape) if o_all is not None else None}
-    launches_per_step = 4  # sample_gather, probe(+select), refine, attention
+    launches_per_step = 4 + int(gt)  # [gt_pool], sample_gather, probe(+select), refine, attention
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws,
@@ -364,6 +452,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (smooth-field Q/K, iid V; DESIGN.md §Inputs)",
             "config": {"workload": w.name, "B_total": ws, "H": w.H, "N": N, "d": d,
+                       "variant": args.variant + (f" (window {args.window})" if gt else ""),
                        "mask": mode, "tau": mp["tau"], "keep": [mp["keep_min"], mp["keep_max"]],
                        "block": 128, "samples": 16, "sparsity": round(float(sparsity), 4),
                        "parallelism": f"(batch,head)-sharded x{ws}, no collective",

@@ -30,7 +30,8 @@
  *     non-OK status means nothing was launched.  Launch failures return
  *     BLADE_ERR_CUDA (cudaGetLastError).  No C++ exception crosses the ABI.
  *   - Non-finite inputs give undefined (but memory-safe) outputs.
- *   - The library is stateless and re-entrant.
+ *   - The device entry points are stateless and re-entrant (the host-buffer
+ *     entry point keeps per-device copy streams, see below).
  *   - GPU limits: block (b) == 128; d in {64, 128}; samples (k) in
  *     {16, 32, 64, 128}; N >= 1; N_b = ceil(N/b) <= 512.  Other values give
  *     BLADE_ERR_UNSUPPORTED.
@@ -126,6 +127,73 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
                              const int32_t* kv_idx, const int32_t* kv_cnt,
                              void* o, float* lse, int32_t impl,
                              void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * ASA with global tokens, ASA_GT (Step 2.2 (2); readings R-18..R-20):
+ * K_aug = Concat(K, MeanPool_n(K)), V_aug likewise.  Window w of the token
+ * axis covers [w*n, min((w+1)*n, N)); N_g = ceil(N/n) global tokens.
+ *
+ * blade_gt_pool — MeanPool_n of K and V.
+ *   k, v        [BH, N, d] bf16 device, 16-byte aligned.
+ *   kg, vg      [BH, N_g, d] bf16 device out, 16-byte aligned: the mean of
+ *               window w's n_w tokens (fp32 sum, rounded once to bf16).
+ *   window      n >= 1.   BH <= 65535.
+ * Errors: INVALID_ARG, UNSUPPORTED (d not in {64, 128}), CUDA.
+ */
+blade_status_t blade_gt_pool(const void* k, const void* v, int64_t BH, int32_t N, int32_t d,
+                             int32_t window, void* kg, void* vg, void* stream);
+
+/*
+ * blade_bsa_gt_fwd — blade_bsa_fwd plus the global tokens, in one softmax:
+ *   LSE[r] = ln( sum_{t in T} e^{s_t} + sum_w e^{g_w} ),
+ *   O[r]   = sum_{t in T} e^{s_t - LSE[r]} v_t + sum_w e^{g_w - LSE[r]} vg_w,
+ *   s_t = scale * q_r . k_t (t in the kept blocks T, as blade_bsa_fwd),
+ *   g_w = scale * q_r . kg_w + ln(n_w)  for every window w (n_w = n except
+ *   possibly the last window).
+ *   kg, vg      [BH, N_g, d] bf16 (e.g. from blade_gt_pool), N_g = ceil(N/n).
+ *   Other arguments and workspace as blade_bsa_fwd (same workspace size).
+ *   impl        BLADE_ATTN_AUTO or BLADE_ATTN_TCGEN05 (MMA_SYNC: UNSUPPORTED).
+ */
+blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                                int32_t N, int32_t d, int32_t block, float scale,
+                                const int32_t* kv_idx, const int32_t* kv_cnt, const void* kg,
+                                const void* vg, int32_t window, void* o, float* lse,
+                                int32_t impl, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+/* Bytes of DEVICE scratch blade_asa_fwd_host needs (0 on bad args / GPU limits). */
+size_t blade_asa_fwd_host_workspace_size(int64_t BH, int32_t N, int32_t d,
+                                         const blade_asa_params_t* params,
+                                         int32_t chunk_units);
+
+/*
+ * blade_asa_fwd_host — the whole ASA forward (blade_asa_mask, then
+ * blade_bsa_fwd; P:138-156 then P:133) on HOST buffers: the units are
+ * streamed through the GPU in chunks of `chunk_units` (0 = auto, about 16
+ * chunks), the host->device copy of chunk c+1, the compute of chunk c and
+ * the device->host copy of chunk c-1 overlapping (units are independent,
+ * P:142-154).  Results equal the two device calls over all units bit for bit
+ * (the sampler is keyed by params->unit_offset + global unit, reading R-1).
+ *   q_host, k_host, v_host  [BH, N, d] bf16 HOST memory (page-locked for
+ *               overlap; pageable memory works but copies synchronously).
+ *   o_host      [BH, N, d] bf16 HOST out (required); lse_host [BH, N] fp32
+ *               HOST out (optional); kv_cnt_host [BH, N_b] int32 HOST out
+ *               (optional).
+ *   workspace   DEVICE scratch >= blade_asa_fwd_host_workspace_size(),
+ *               256-byte aligned: two chunk slots of Q/K/V/O/LSE/lists plus
+ *               the mask and attention scratch.
+ *   stream      compute runs on it; when it completes, every host output is
+ *               written.  The host must not touch the host buffers before.
+ * State: two non-blocking copy streams and a few events per device, created
+ * on first use and kept for the process; concurrent calls on one device are
+ * serialised while enqueuing.  Errors: as blade_asa_mask / blade_bsa_fwd.
+ */
+blade_status_t blade_asa_fwd_host(const void* q_host, const void* k_host, const void* v_host,
+                                  int64_t BH, int32_t N, int32_t d,
+                                  const blade_asa_params_t* params, int32_t impl,
+                                  int32_t chunk_units, void* o_host, float* lse_host,
+                                  int32_t* kv_cnt_host, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 
 /* Static, NUL-terminated description of a status code. */
 const char* blade_status_string(blade_status_t status);

@@ -30,7 +30,9 @@ BLADE_OK, BLADE_ERR_INVALID_ARG, BLADE_ERR_UNSUPPORTED, BLADE_ERR_WORKSPACE, BLA
 ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC = 0, 1, 2
 
 ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd_workspace_size",
-               "blade_bsa_fwd", "blade_status_string", "blade_version")
+               "blade_bsa_fwd", "blade_gt_pool", "blade_bsa_gt_fwd",
+               "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
+               "blade_status_string", "blade_version")
 
 
 class BladeAsaParams(ctypes.Structure):
@@ -55,6 +57,18 @@ _lib.blade_bsa_fwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
 _lib.blade_bsa_fwd.restype = ctypes.c_int
 _lib.blade_bsa_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp, _vp,
                                _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_gt_pool.restype = ctypes.c_int
+_lib.blade_gt_pool.argtypes = [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]
+_lib.blade_bsa_gt_fwd.restype = ctypes.c_int
+_lib.blade_bsa_gt_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp,
+                                  _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_asa_fwd_host_workspace_size.restype = _sz
+_lib.blade_asa_fwd_host_workspace_size.argtypes = [_i64, _i32, _i32,
+                                                   ctypes.POINTER(BladeAsaParams), _i32]
+_lib.blade_asa_fwd_host.restype = ctypes.c_int
+_lib.blade_asa_fwd_host.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32,
+                                    ctypes.POINTER(BladeAsaParams), _i32, _i32, _vp, _vp, _vp,
+                                    _vp, _sz, _vp]
 _lib.blade_status_string.restype = ctypes.c_char_p
 _lib.blade_status_string.argtypes = [ctypes.c_int]
 _lib.blade_version.restype = _i32
@@ -209,6 +223,116 @@ def blade_bsa_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_idx: tor
                             _stream(stream))
     if st != BLADE_OK:
         raise BladeError(st, "blade_bsa_fwd")
+    return o, lse
+
+
+def num_global_tokens(N: int, window: int) -> int:
+    """N_g = ceil(N / n) (reading R-18)."""
+    return (N + window - 1) // window
+
+
+def blade_gt_pool(k: torch.Tensor, v: torch.Tensor, *, window: int = 128,
+                  kg: torch.Tensor | None = None, vg: torch.Tensor | None = None, stream=None):
+    """MeanPool_n of K and V -> (K_g, V_g) bf16 [BH, N_g, d]."""
+    k = _as_units(k, "k")
+    v = _as_units(v, "v")
+    BH, N, d = k.shape
+    Ng = num_global_tokens(N, window)
+    if kg is None:
+        kg = torch.empty((BH, Ng, d), dtype=torch.bfloat16, device=k.device)
+    if vg is None:
+        vg = torch.empty((BH, Ng, d), dtype=torch.bfloat16, device=k.device)
+    st = _lib.blade_gt_pool(_ptr(k), _ptr(v), BH, N, d, window, _ptr(kg), _ptr(vg),
+                            _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_gt_pool")
+    return kg, vg
+
+
+def blade_bsa_gt_fwd(q, k, v, kv_idx, kv_cnt, kg, vg, *, window: int = 128,
+                     scale: float | None = None, block: int = 128, impl: int = ATTN_AUTO,
+                     want_lse: bool = True, o=None, lse=None, stream=None):
+    """ASA_GT attention: kept blocks plus every global token with the
+    ln(n_w) bias, one softmax -> (O, LSE)."""
+    q = _as_units(q, "q")
+    k = _as_units(k, "k")
+    v = _as_units(v, "v")
+    BH, N, d = q.shape
+    Ng = num_global_tokens(N, window)
+    for t, nm in ((kg, "kg"), (vg, "vg")):
+        if (t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous()
+                or tuple(t.shape) != (BH, Ng, d)):
+            raise ValueError(f"{nm} must be contiguous CUDA bf16 of shape {(BH, Ng, d)}")
+    if o is None:
+        o = torch.empty_like(q)
+    if lse is None and want_lse:
+        lse = torch.empty((BH, N), dtype=torch.float32, device=q.device)
+    nbytes = _lib.blade_bsa_fwd_workspace_size(BH, N, d, block)
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_fwd_workspace_size")
+    ws = _workspace(nbytes, q.device, "attn")
+    st = _lib.blade_bsa_gt_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, block,
+                               default_scale(d) if scale is None else scale, _ptr(kv_idx),
+                               _ptr(kv_cnt), _ptr(kg), _ptr(vg), window, _ptr(o), _ptr(lse),
+                               impl, _ptr(ws), ws.numel(), _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_bsa_gt_fwd")
+    return o, lse
+
+
+def asa_gt_forward(q, k, v, *, window: int = 128, tau: float = 0.9, keep_min: int = 1,
+                   keep_max: int = 1 << 30, samples: int = 16, seed: int = 42,
+                   unit_offset: int = 0, stream=None, **mask_kw):
+    """ASA_GT forward: MeanPool_n, mask generation (Alg. 1, unchanged by the
+    global tokens, reading R-20), then attention.  Returns (O, LSE, MaskOut)."""
+    kg, vg = blade_gt_pool(k, v, window=window, stream=stream)
+    m = blade_asa_mask(q, k, tau=tau, keep_min=keep_min, keep_max=keep_max, samples=samples,
+                       seed=seed, unit_offset=unit_offset, stream=stream, **mask_kw)
+    o, lse = blade_bsa_gt_fwd(q, k, v, m.kv_idx, m.kv_cnt, kg, vg, window=window, stream=stream)
+    return o, lse, m
+
+
+def _as_host_units(x: torch.Tensor, name: str) -> torch.Tensor:
+    if x.dim() == 4:
+        x = x.reshape(-1, x.shape[2], x.shape[3])
+    if x.dim() != 3 or x.dtype != torch.bfloat16 or x.is_cuda or not x.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous host (CPU) bf16 [B,H,N,d] or [BH,N,d] tensor")
+    return x
+
+
+def blade_asa_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, tau: float = 0.9,
+                       keep_min: int = 1, keep_max: int = 1 << 30, samples: int = 16,
+                       seed: int = 42, unit_offset: int = 0, impl: int = ATTN_AUTO,
+                       chunk_units: int = 0, o: torch.Tensor | None = None,
+                       lse: torch.Tensor | None = None, want_lse: bool = True,
+                       kv_cnt: torch.Tensor | None = None, device: torch.device | None = None,
+                       stream=None, **mask_kw):
+    """The whole ASA forward on HOST (preferably pinned) tensors, chunked over
+    units with copy/compute overlap (blade_asa_fwd_host).  Enqueued on
+    ``stream`` of ``device``; outputs are valid once that stream completes.
+    Returns (O, LSE) as host tensors."""
+    q = _as_host_units(q, "q")
+    k = _as_host_units(k, "k")
+    v = _as_host_units(v, "v")
+    BH, N, d = q.shape
+    if k.shape != q.shape or v.shape != q.shape:
+        raise ValueError("q, k, v shapes differ")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    prm = make_params(d=d, tau=tau, keep_min=keep_min, keep_max=keep_max, samples=samples,
+                      seed=seed, unit_offset=unit_offset, **mask_kw)
+    if o is None:
+        o = torch.empty_like(q).pin_memory()
+    if lse is None and want_lse:
+        lse = torch.empty((BH, N), dtype=torch.float32).pin_memory()
+    nbytes = _lib.blade_asa_fwd_host_workspace_size(BH, N, d, ctypes.byref(prm), chunk_units)
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_asa_fwd_host_workspace_size")
+    ws = _workspace(nbytes, dev, "host")
+    st = _lib.blade_asa_fwd_host(_ptr(q), _ptr(k), _ptr(v), BH, N, d, ctypes.byref(prm), impl,
+                                 chunk_units, _ptr(o), _ptr(lse), _ptr(kv_cnt), _ptr(ws),
+                                 ws.numel(), _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_asa_fwd_host")
     return o, lse
 
 

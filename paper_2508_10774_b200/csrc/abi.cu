@@ -55,6 +55,13 @@ blade_status_t make_mask_problem(int64_t BH, int32_t N, int32_t d,
 
 }  // namespace
 
+namespace blade {
+int validate_mask_params(int64_t BH, int32_t N, int32_t d, const blade_asa_params_t* prm) {
+  MaskProblem p;
+  return int(make_mask_problem(BH, N, d, prm, &p));
+}
+}  // namespace blade
+
 extern "C" {
 
 size_t blade_asa_mask_workspace_size(int64_t BH, int32_t N, int32_t d,
@@ -119,6 +126,46 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
       e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
     }
   }
+  return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+
+blade_status_t blade_gt_pool(const void* k, const void* v, int64_t BH, int32_t N, int32_t d,
+                             int32_t window, void* kg, void* vg, void* stream) {
+  if (!k || !v || !kg || !vg) return BLADE_ERR_INVALID_ARG;
+  if (!aligned16(k) || !aligned16(v) || !aligned16(kg) || !aligned16(vg)) return BLADE_ERR_INVALID_ARG;
+  if (BH < 1 || BH > 65535 || N < 1 || window < 1) return BLADE_ERR_INVALID_ARG;
+  if (d != 64 && d != 128) return BLADE_ERR_UNSUPPORTED;
+  cudaError_t e = blade::launch_gt_pool(k, v, BH, N, d, window, kg, vg,
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+
+blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                                int32_t N, int32_t d, int32_t block, float scale,
+                                const int32_t* kv_idx, const int32_t* kv_cnt, const void* kg,
+                                const void* vg, int32_t window, void* o, float* lse,
+                                int32_t impl, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  if (!q || !k || !v || !kv_idx || !kv_cnt || !o || !kg || !vg) return BLADE_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(kg) ||
+      !aligned16(vg))
+    return BLADE_ERR_INVALID_ARG;
+  if (BH < 1 || N < 1 || block < 1 || window < 1 || !(scale > 0.f) || !isfinite(scale))
+    return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_MMA_SYNC) return BLADE_ERR_INVALID_ARG;
+  if (block != kGpuBlock || (d != 64 && d != 128) || impl == BLADE_ATTN_MMA_SYNC)
+    return BLADE_ERR_UNSUPPORTED;
+  const int64_t Nb = (int64_t(N) + block - 1) / block;
+  if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
+  AttnProblem p{BH, N, d, block, int(Nb), scale};
+  const size_t need = blade_bsa_fwd_workspace_size(BH, N, d, block);
+  if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return BLADE_ERR_WORKSPACE;
+  const blade::GtProblem g{kg, vg, int((int64_t(N) + window - 1) / window), int(window)};
+  cudaError_t e = blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
+                                        static_cast<char*>(workspace), workspace_bytes,
+                                        static_cast<cudaStream_t>(stream), &g);
+  if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
 }
 

@@ -132,12 +132,23 @@ __device__ unsigned long long g_tm[10];
 #define TM_ADD(i, v) atomicAdd(&g_tm[i], (unsigned long long)(v))
 #endif
 
-template <int D, bool kDefaultScale>
+// Global tokens of ASA_GT: N_g pooled K/V rows attended by every
+// query after its kept blocks, as ceil(N_g/128) extra tiles with the additive
+// bias ln(n_w) (readings R-18..R-20), applied in raw-score units (/ scale).
+struct GtArgs {
+  int Ng;             // number of global tokens (0: plain ASA)
+  float bias_full;    // ln(n) / scale      (full windows)
+  float bias_last;    // ln(n_last) / scale (the last, possibly partial, window)
+};
+
+template <int D, bool kDefaultScale, bool kGT>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, int N, int Nb, float scale_log2_rt,
-                   const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
-                   __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, volatile int* dbg) {
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmKg,
+                   const __grid_constant__ CUtensorMap tmVg, const GtArgs gt, int N, int Nb,
+                   float scale_log2_rt, const int32_t* __restrict__ kv_idx,
+                   const int32_t* __restrict__ kv_cnt, __nv_bfloat16* __restrict__ O,
+                   float* __restrict__ LSE, volatile int* dbg) {
   using C = Cfg<D>;
   const float scale_log2 = kDefaultScale ? DefaultScale<D>::kScaleLog2 : scale_log2_rt;
 #ifdef BLADE_TC_DEBUG
@@ -167,7 +178,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int i = blockIdx.x;
   const int64_t u = blockIdx.y;
   const int64_t row_id = u * Nb + i;
-  const int cnt = kv_cnt[row_id];
+  const int cnt_fine = kv_cnt[row_id];
+  // items: the kept blocks, then (ASA_GT) the global-token tiles
+  const int cnt = cnt_fine + (kGT ? (gt.Ng + 127) / 128 : 0);
   const int32_t* list = kv_idx + row_id * Nb;
 
   if (warp == 5 && lane == 0) {
@@ -201,11 +214,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (isK) {
         tc::tma_prefetch_desc(&tmQ);
         tc::tma_prefetch_desc(&tmK);
+        if (kGT) tc::tma_prefetch_desc(&tmKg);
         tc::mbar_arrive_expect_tx(bar_q, C::kTile);
         for (int p = 0; p < C::kPanels; ++p)
           tc::tma_load_3d(sQ + p * C::kPanel, &tmQ, bar_q, p * 64, i * 128, int(u));
       } else {
         tc::tma_prefetch_desc(&tmV);
+        if (kGT) tc::tma_prefetch_desc(&tmVg);
       }
       const int R = isK ? C::kRingK : C::kRingVx;
       char* ring = isK ? sRingK : sRingV;
@@ -217,12 +232,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       // warm L2 for the first blocks, then keep BLADE_ATTN_L2_PREFETCH blocks
       // ahead of the ring: a block's first touch comes from HBM
-      for (int n = 0; n < BLADE_ATTN_L2_PREFETCH && n < cnt; ++n)
+      for (int n = 0; n < BLADE_ATTN_L2_PREFETCH && n < cnt_fine; ++n)
         for (int p = 0; p < C::kPanels; ++p) tc::tma_prefetch_3d(m, p * 64, list[n] * 128, int(u));
       for (int n = 0; n < cnt; ++n) {
         const int s = n % R;
         TC_DBG(0, n);
-        if (BLADE_ATTN_L2_PREFETCH > 0 && n + BLADE_ATTN_L2_PREFETCH < cnt)
+        if (BLADE_ATTN_L2_PREFETCH > 0 && n + BLADE_ATTN_L2_PREFETCH < cnt_fine)
           for (int p = 0; p < C::kPanels; ++p)
             tc::tma_prefetch_3d(m, p * 64, list[n + BLADE_ATTN_L2_PREFETCH] * 128, int(u));
 #ifdef BLADE_ATTN_TIMING
@@ -242,9 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           dst = sQ;
         }
         tc::mbar_arrive_expect_tx(full + s, C::kTile);
-        const int j = list[n];
+        const bool fine = !kGT || n < cnt_fine;
+        const CUtensorMap* mm = fine ? m : (isK ? &tmKg : &tmVg);
+        const int row0 = fine ? list[n] * 128 : (n - cnt_fine) * 128;
         for (int p = 0; p < C::kPanels; ++p)
-          tc::tma_load_3d(dst + p * C::kPanel, m, full + s, p * 64, j * 128, int(u));
+          tc::tma_load_3d(dst + p * C::kPanel, mm, full + s, p * 64, row0, int(u));
 #endif
       }
     }
@@ -380,11 +397,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           s[96 + e] = __uint_as_float(r3[e]);
         }
       }
-      const int valid = N - list[n] * 128;  // keys of the (possibly partial) last block
+      const bool fine = !kGT || n < cnt_fine;
+      // keys of the (possibly partial) last block / global-token tile
+      const int valid = fine ? N - list[n] * 128 : gt.Ng - (n - cnt_fine) * 128;
       if (valid < 128) {
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (c >= valid) s[c] = -INFINITY;
+      }
+      if (kGT && !fine) {  // + ln(n_w) on the pooled region, raw-score units
+        const int last = gt.Ng - 1 - (n - cnt_fine) * 128;  // column of the last window
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] += c == last ? gt.bias_last : gt.bias_full;
       }
       // row max as a tree (a linear chain would serialise 64 ALU latencies)
       float mx;
@@ -503,14 +527,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D>
 cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                      const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                     cudaStream_t stream) {
-  CUtensorMap mq, mk, mv;
+                     const GtProblem* g, cudaStream_t stream) {
+  CUtensorMap mq, mk, mv, mkg, mvg;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mk, k, p.BH, p.N, D) ||
       !make_tile_map(&mv, v, p.BH, p.N, D))
     return cudaErrorNotSupported;
+  GtArgs ga{0, 0.f, 0.f};
+  if (g) {
+    if (!make_tile_map(&mkg, g->kg, p.BH, g->Ng, D) || !make_tile_map(&mvg, g->vg, p.BH, g->Ng, D))
+      return cudaErrorNotSupported;
+    const int n_last = p.N - (g->Ng - 1) * g->window;
+    ga.Ng = g->Ng;
+    ga.bias_full = logf(float(g->window)) / p.scale;
+    ga.bias_last = logf(float(n_last)) / p.scale;
+  } else {
+    mkg = mk;
+    mvg = mv;
+  }
   constexpr int smem = Cfg<D>::kSmem;
   const bool dflt = p.scale == (D == 128 ? 0.088388346f : 0.125f);
-  auto kern = dflt ? attn_tc_kernel<D, true> : attn_tc_kernel<D, false>;
+  auto kern = g ? (dflt ? attn_tc_kernel<D, true, true> : attn_tc_kernel<D, false, true>)
+                : (dflt ? attn_tc_kernel<D, true, false> : attn_tc_kernel<D, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(p.Nb), unsigned(p.BH));
@@ -524,7 +561,7 @@ cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const v
   cudaHostGetDevicePointer(&dbg_dev, dbg_host, 0);
 #endif
   kern<<<grid, kThreads, smem, stream>>>(
-      mq, mk, mv, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
+      mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
       reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev);
   e = cudaGetLastError();
 #ifdef BLADE_ATTN_TRACE
@@ -580,9 +617,9 @@ size_t attn_tc_workspace(const AttnProblem&) { return 256; }
 
 cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                            const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                           char*, size_t, cudaStream_t stream) {
-  if (p.d == 64) return launch_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, stream);
-  if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, stream);
+                           char*, size_t, cudaStream_t stream, const GtProblem* gt) {
+  if (p.d == 64) return launch_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
+  if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
   return cudaErrorNotSupported;
 }
 

@@ -82,11 +82,22 @@ cudaError_t launch_attn_mma(const AttnProblem& p, const void* q, const void* k,
                             const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
                             void* o, float* lse, cudaStream_t stream);
 
+// ASA_GT global tokens: pooled K/V [BH, Ng, d] bf16 and the window n.
+struct GtProblem {
+  const void* kg;
+  const void* vg;
+  int Ng, window;
+};
+
 // Returns cudaErrorNotSupported when the tcgen05 path is not available.
 cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k,
                            const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
                            void* o, float* lse, char* ws, size_t ws_bytes,
-                           cudaStream_t stream);
+                           cudaStream_t stream, const GtProblem* gt = nullptr);
+
+// MeanPool_n of K and V, fp32 accumulation, bf16 round-to-nearest.
+cudaError_t launch_gt_pool(const void* k, const void* v, int64_t BH, int N, int d, int window,
+                           void* kg, void* vg, cudaStream_t stream);
 size_t attn_tc_workspace(const AttnProblem& p);
 
 }  // namespace blade

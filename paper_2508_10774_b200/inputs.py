@@ -132,3 +132,28 @@ def make(workload: str | Workload, recipe: str = "smooth", seed: int = 42,
         return smooth(Bv, w.H, w.N, w.d, w.grid, w.n_text, w.ell, w.beta,
                       w.sigma_n, seed)
     raise ValueError(recipe)
+
+
+def smooth_device(units: int, N: int, d: int, grid: tuple, device, n_text: int = 0,
+                  ell: float = 3.0, beta: float = 9.0, sigma_n: float = 0.1, seed: int = 42):
+    """The ``smooth`` recipe drawn with torch's CUDA generator directly on the
+    device (same distribution, different stream of random numbers than the
+    numpy version), for workloads too large to generate on the host (the
+    30-layer batch-8 stack, BASELINE.json configs[4]).  Returns bf16
+    [units, N, d] q, k, v on ``device``."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    pos = torch.from_numpy(grid_positions(grid)).to(device)
+    q = torch.empty((units, N, d), dtype=torch.bfloat16, device=device)
+    k = torch.empty_like(q)
+    for u in range(units):
+        W = torch.randn((3, d), generator=g, device=device) / ell
+        phi = torch.rand(d, generator=g, device=device) * (2 * np.pi)
+        F = (2.0 / d) ** 0.5 * torch.cos(pos @ W + phi)
+        if n_text:
+            T = torch.randn((n_text, d), generator=g, device=device) / d ** 0.5
+            F = torch.cat([T, F], 0)
+        q[u] = beta * F + sigma_n * torch.randn((N, d), generator=g, device=device)
+        k[u] = beta * F + sigma_n * torch.randn((N, d), generator=g, device=device)
+    v = torch.randn((units, N, d), generator=g, device=device).to(torch.bfloat16)
+    return q, k, v

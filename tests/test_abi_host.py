@@ -110,3 +110,53 @@ def test_keep_count_integer_rounding(asa):
     assert asa.keep_count(50_000, 256) == 13          # ceil(0.05 * 256)
     assert asa.keep_count(200_000, 256) == 52
     assert asa.keep_count(1, 4) == 1
+
+
+def test_host_pipeline_validation_codes(asa):
+    A, lib = asa, asa._lib
+    P = 1 << 20
+    prm = A.make_params(d=64)
+
+    def call(q=P, o=P, BH=2, N=512, d=64, impl=0, chunk=0, ws=P, wsb=1 << 40, p=prm):
+        return lib.blade_asa_fwd_host(q, P, P, BH, N, d, ctypes.byref(p), impl, chunk, o, None,
+                                      None, ws, wsb, None)
+
+    assert call(q=None) == A.BLADE_ERR_INVALID_ARG
+    assert call(o=None) == A.BLADE_ERR_INVALID_ARG
+    assert call(BH=0) == A.BLADE_ERR_INVALID_ARG
+    assert call(chunk=-1) == A.BLADE_ERR_INVALID_ARG
+    assert call(impl=9) == A.BLADE_ERR_INVALID_ARG
+    assert call(p=A.make_params(d=64, tau=2.0)) == A.BLADE_ERR_INVALID_ARG
+    assert call(d=80, p=A.make_params(d=80)) == A.BLADE_ERR_UNSUPPORTED
+    assert call(ws=None) == A.BLADE_ERR_WORKSPACE
+    assert call(wsb=16) == A.BLADE_ERR_WORKSPACE
+
+
+def test_host_pipeline_workspace_scales_with_chunk(asa):
+    lib = asa._lib
+    p = asa.make_params(d=128)
+    w1 = lib.blade_asa_fwd_host_workspace_size(12, 32760, 128, ctypes.byref(p), 1)
+    w3 = lib.blade_asa_fwd_host_workspace_size(12, 32760, 128, ctypes.byref(p), 3)
+    tok = 32760 * 128 * 2
+    assert w1 >= 2 * 4 * tok  # two slots of Q, K, V, O for one unit
+    assert w3 >= 2 * 4 * 3 * tok and w3 > w1
+    assert lib.blade_asa_fwd_host_workspace_size(12, 32760, 128, ctypes.byref(p), 0) == w1
+
+
+def test_gt_validation_codes(asa):
+    A, lib = asa, asa._lib
+    P = 1 << 20
+    assert lib.blade_gt_pool(None, P, 1, 512, 64, 128, P, P, None) == A.BLADE_ERR_INVALID_ARG
+    assert lib.blade_gt_pool(P, P, 1, 512, 64, 0, P, P, None) == A.BLADE_ERR_INVALID_ARG
+    assert lib.blade_gt_pool(P, P, 1, 512, 64, 128, P + 4, P, None) == A.BLADE_ERR_INVALID_ARG
+    assert lib.blade_gt_pool(P, P, 1, 512, 96, 128, P, P, None) == A.BLADE_ERR_UNSUPPORTED
+
+    def call(kg=P, window=128, impl=0, d=64, ws=P):
+        return lib.blade_bsa_gt_fwd(P, P, P, 1, 512, d, 128, 0.125, P, P, kg, P, window, P, None,
+                                    impl, ws, 1 << 40, None)
+
+    assert call(kg=None) == A.BLADE_ERR_INVALID_ARG
+    assert call(window=0) == A.BLADE_ERR_INVALID_ARG
+    assert call(impl=A.ATTN_MMA_SYNC) == A.BLADE_ERR_UNSUPPORTED
+    assert call(d=256) == A.BLADE_ERR_UNSUPPORTED
+    assert call(ws=None) == A.BLADE_ERR_WORKSPACE
