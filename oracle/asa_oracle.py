@@ -273,7 +273,8 @@ def select_row(p_row: np.ndarray, tau: float, lo: int, hi: int) -> RowSelection:
     l.7  p~_j = P_imp(i, j) / sum_k P_imp(i, k)   (sum ascending j, fp64)
     l.8  sort descending (reading R-7: ties -> lower block id first)
     l.9  smallest m with sum_{r<=m} s_r >= tau (reading R-4: '>=', Alg. 1,
-         not 'exceed' of P:124; if never reached, m0 = N_b), then clamp m to
+         not 'exceed' of P:124; if never reached, m0 = N_b; tau = 1 gives
+         m0 = N_b, "tau = 1 -> dense"), then clamp m to
          [lo, hi] (reading R-6: integer clamps)
     l.10 M[i, j] = 1 for the top m indices.
     """
@@ -288,10 +289,11 @@ def select_row(p_row: np.ndarray, tau: float, lo: int, hi: int) -> RowSelection:
         c += phat[j]
         csum.append(c)
     m0 = Nb
-    for r in range(Nb):
-        if csum[r] >= tau:
-            m0 = r + 1
-            break
+    if tau < 1.0:  # reading R-4: tau = 1 keeps all N_b blocks (exact mass of
+        for r in range(Nb):  # positive scores reaches 1 only at N_b, whatever fp64 rounding says)
+            if csum[r] >= tau:
+                m0 = r + 1
+                break
     m = min(max(m0, lo), hi)
     return RowSelection(phat, order, csum, m0, m, sorted(order[:m]))
 
@@ -427,7 +429,7 @@ def tie_exemption(sel: RowSelection, tau: float, lo: int, hi: int,
     clamp = lambda x: min(max(x, lo), hi)
     counts = {sel.m}
     t1 = False
-    for mp in (sel.m0 - 1, sel.m0):
+    for mp in ((sel.m0 - 1, sel.m0) if tau < 1.0 else ()):  # tau = 1: no cut (R-4)
         if 1 <= mp <= Nb and abs(sel.csum[mp - 1] - tau) <= eps * tau:
             for alt in (mp, mp + 1):
                 if 1 <= alt <= Nb and clamp(alt) != sel.m:

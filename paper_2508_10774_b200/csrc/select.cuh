@@ -2,7 +2,7 @@
 //
 //   l.7   p~_j = P_imp(i,j) / sum_k P_imp(i,k)                (fp64)
 //   l.8   sort p~ descending, ties by ascending block id       (reading R-7)
-//   l.9   m0 = smallest m with sum_{r<=m} s_r >= tau, else N_b (reading R-4),
+//   l.9   m0 = smallest m with sum_{r<=m} s_r >= tau, else N_b; N_b for tau = 1 (R-4),
 //         m  = clamp(m0, lo, hi)                               (reading R-6)
 //   l.10  M[i, j] = 1 for the top m; compacted to ascending kv_idx
 //
@@ -117,7 +117,9 @@ struct RowSelect {
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    const int m0 = first <= Nb ? first : Nb;
+    // tau >= 1 keeps every block (reading R-4: exact cumulative mass of positive
+    // scores reaches 1 only at N_b); else the first m with C_m >= tau
+    const int m0 = (tau >= 1.0 || first > Nb) ? Nb : first;
     const int m = min(max(m0, lo), hi);
 
     bool flag = false;
@@ -143,7 +145,7 @@ struct RowSelect {
       const double cm0 = getC(m0 - 1), cm1 = getC(m0 - 2);
       const double band = guard * tau;
       auto clampi = [&](int x) { return min(max(x, lo), hi); };
-      const bool cut_matters = clampi(m0 - 1) != m || clampi(m0 + 1) != m;
+      const bool cut_matters = tau < 1.0 && (clampi(m0 - 1) != m || clampi(m0 + 1) != m);
       if (cut_matters && (fabs(cm0 - tau) <= band || (m0 >= 2 && fabs(cm1 - tau) <= band)))
         flag = true;
       if (m < Nb) {
@@ -267,7 +269,9 @@ struct RowSelectF32 {
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    const int m0 = first <= Nb ? first : Nb;
+    // tau >= 1 keeps every block (reading R-4: exact cumulative mass of positive
+    // scores reaches 1 only at N_b); else the first m with C_m >= tau
+    const int m0 = (tau >= 1.0 || first > Nb) ? Nb : first;
     const int m = min(max(m0, lo), hi);
     bool flag = false;
     if (want_flag) {
@@ -282,7 +286,7 @@ struct RowSelectF32 {
       const double cm1 = m0 >= 2 ? pick(c, m0 - 2) : 0.0;
       const double band = guard * tau;
       auto clampi = [&](int x) { return min(max(x, lo), hi); };
-      const bool cut_matters = clampi(m0 - 1) != m || clampi(m0 + 1) != m;
+      const bool cut_matters = tau < 1.0 && (clampi(m0 - 1) != m || clampi(m0 + 1) != m);
       if (cut_matters && (fabs(cm0 - tau) <= band || (m0 >= 2 && fabs(cm1 - tau) <= band)))
         flag = true;
       if (m < Nb) {

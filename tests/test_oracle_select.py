@@ -142,3 +142,17 @@ def test_non_exempt_mismatch_is_rejected():
     sel = O.select_row(np.array([0.5, 0.3, 0.15, 0.05]), 0.9, 1, 4)
     assert O.check_row_against(sel, 0.9, 1, 4, [0, 1]) is not None
     assert O.check_row_against(sel, 0.9, 1, 4, [0, 1, 2]) is None
+
+
+def test_tau_one_is_dense_even_when_fp64_sum_saturates():
+    """S:259 'tau = 1 -> dense': with every score positive the exact
+    cumulative mass reaches 1 only at N_b, although the fp64 running sum of
+    [1, 1e-20, 1e-20] already equals 1.0 after the first term."""
+    row = np.array([1.0, 1e-20, 1e-20, 1e-30])
+    sel = O.select_row(row, 1.0, 1, 4)
+    assert sel.csum[0] == 1.0           # the fp64 sum saturates at m = 1 ...
+    assert sel.m0 == 4 and sel.m == 4   # ... but tau = 1 keeps every block
+    assert sel.kept == [0, 1, 2, 3]
+    assert O.select_row(row, 1.0, 1, 2).m == 2          # the clamp still applies
+    te = O.tie_exemption(sel, 1.0, 1, 4)
+    assert not te["t1"]
