@@ -61,12 +61,27 @@ struct Cfg {
   static constexpr int kRingVx = kRingV + 1;
   static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingVx + 5 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
-  static constexpr int kSmem = kOffMisc + 16 + 1024;  // + alignment slack
+  // row-max exchange between the two column halves of a row (bf16, rounded
+  // up): [S buffer][half][row]; reused for the final l exchange (fp32)
+  static constexpr int kOffXch = kOffMisc + 16;
+  static constexpr int kSmem = kOffXch + 1024 + 1024;  // + alignment slack
   static constexpr uint32_t kColO = 256;
   static constexpr uint32_t kColQ = 256 + D;  // Q in TMEM (bf16 pairs): D / 2 columns
 };
 
-constexpr int kThreads = 256;
+// Softmax warps: kSplit x 4.  With kSplit = 2 each query row is shared by two
+// warps (one per 64-column half of S, same TMEM lane quarter): twice the
+// warps to hide the softmax's latency chain (ld -> max -> exp -> st -> arrive)
+// at the cost of one row-max exchange per tile.
+#ifndef BLADE_ATTN_SPLIT
+#define BLADE_ATTN_SPLIT 1  // 2 measured slower on B200 (Wan 1.252 vs 1.231 ms, Cog 1.221 vs 1.133 ms)
+#endif
+constexpr int kSplit = BLADE_ATTN_SPLIT;
+constexpr int kSoftWarps = 4 * kSplit;
+constexpr int kMmaWarp = kSoftWarps;      // tcgen05.mma issuer + TMEM allocator
+constexpr int kLoadKWarp = kSoftWarps + 1;  // TMA: Q, then K
+constexpr int kLoadVWarp = kSoftWarps + 2;  // TMA: V
+constexpr int kThreads = 32 * (kSoftWarps + 3);
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P may reach 2^8 before O is rescaled
 // which of every 8 exponential PAIRS run on the FMA pipe (bit k: pair k)
 #ifndef BLADE_ATTN_EMU_MASK
@@ -183,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cnt = cnt_fine + (kGT ? (gt.Ng + 127) / 128 : 0);
   const int32_t* list = kv_idx + row_id * Nb;
 
-  if (warp == 5 && lane == 0) {
+  if (warp == kLoadKWarp && lane == 0) {
     tc::mbar_init(bar_q, 1);
     for (int s = 0; s < C::kRingK; ++s) {
       tc::mbar_init(bar_kfull + s, 1);
@@ -195,22 +210,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::mbar_init(bar_s + 0, 1);
     tc::mbar_init(bar_s + 1, 1);
-    tc::mbar_init(bar_p + 0, 4);
-    tc::mbar_init(bar_p + 1, 4);
+    tc::mbar_init(bar_p + 0, kSoftWarps);
+    tc::mbar_init(bar_p + 1, kSoftWarps);
     tc::mbar_init(bar_pv, 1);
     tc::mbar_init(bar_qt, 4);
     tc::fence_barrier_init();
   }
-  if (warp == 4) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) tc::tmem_alloc<512>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5 || warp == 6) {
+  if (warp == kLoadKWarp || warp == kLoadVWarp) {
     // ===================== TMA producers (warp 5: Q and K, warp 6: V) ========
     if (lane == 0) {
-      const bool isK = warp == 5;
+      const bool isK = warp == kLoadKWarp;
       if (isK) {
         tc::tma_prefetch_desc(&tmQ);
         tc::tma_prefetch_desc(&tmK);
@@ -265,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
@@ -335,12 +350,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(bar_pv, (cnt - 1) & 1);
       TC_DBG(1, 5001);
     }
-  } else if (warp < 4) {
+  } else if (warp < kSoftWarps) {
     // ===================== softmax =====================
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
-    const uint32_t tO = tmem + lane_base + C::kColO;
-    {  // Q row (this thread's) from the swizzled smem tile into TMEM columns
-      const int r = warp * 32 + lane;
+    // warp = (half h, lane quarter qw): rows 32 qw + lane, S columns
+    // [h CW, (h+1) CW) of each tile, O columns [h D/kSplit, (h+1) D/kSplit)
+    constexpr int CW = 128 / kSplit;    // S columns per thread
+    constexpr int DW = D / kSplit;      // O columns per thread
+    const int qw = warp & 3, h = warp >> 2;
+    const uint32_t lane_base = uint32_t(qw * 32) << 16;
+    const uint32_t tO = tmem + lane_base + C::kColO + h * DW;
+    const int r = qw * 32 + lane;  // row within the query block
+    uint16_t* xch = reinterpret_cast<uint16_t*>(smem + C::kOffXch);  // [2][2][128]
+    if (h == 0) {  // Q row (this thread's) from the swizzled smem tile into TMEM columns
       tc::mbar_wait(bar_q, 0);
 #pragma unroll
       for (int p = 0; p < C::kPanels; ++p) {
@@ -365,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int n = 0; n < cnt; ++n) {
       const int buf = n & 1;
       const uint32_t tS = tmem + lane_base + buf * 128;
-      if (lane == 0) TC_DBG(2 + warp, 10 * n + 1);
+      if (lane == 0) TC_DBG(2 + (warp & 3), 10 * n + 1);
 #ifdef BLADE_ATTN_TIMING
       const long long tw0 = clock64();
 #endif
@@ -381,36 +402,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc::mbar_arrive(bar_p + buf);
       continue;
 #endif
-      float s[128];
-      {
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        tc::ld_32x32b_x32(tS + 0, r0);
-        tc::ld_32x32b_x32(tS + 32, r1);
-        tc::ld_32x32b_x32(tS + 64, r2);
-        tc::ld_32x32b_x32(tS + 96, r3);
+      float s[CW];
+#pragma unroll
+      for (int c = 0; c < CW / 32; ++c) {
+        uint32_t rr[32];
+        tc::ld_32x32b_x32(tS + h * CW + c * 32, rr);
         tc::wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          s[e] = __uint_as_float(r0[e]);
-          s[32 + e] = __uint_as_float(r1[e]);
-          s[64 + e] = __uint_as_float(r2[e]);
-          s[96 + e] = __uint_as_float(r3[e]);
-        }
+        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
       }
       const bool fine = !kGT || n < cnt_fine;
       // keys of the (possibly partial) last block / global-token tile
-      const int valid = fine ? N - list[n] * 128 : gt.Ng - (n - cnt_fine) * 128;
-      if (valid < 128) {
+      const int valid = (fine ? N - list[n] * 128 : gt.Ng - (n - cnt_fine) * 128) - h * CW;
+      if (valid < CW) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
+        for (int c = 0; c < CW; ++c)
           if (c >= valid) s[c] = -INFINITY;
       }
       if (kGT && !fine) {  // + ln(n_w) on the pooled region, raw-score units
-        const int last = gt.Ng - 1 - (n - cnt_fine) * 128;  // column of the last window
+        const int last = gt.Ng - 1 - (n - cnt_fine) * 128 - h * CW;  // column of the last window
 #pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] += c == last ? gt.bias_last : gt.bias_full;
+        for (int c = 0; c < CW; ++c) s[c] += c == last ? gt.bias_last : gt.bias_full;
       }
-      // row max as a tree (a linear chain would serialise 64 ALU latencies)
+      // row max as a tree (a linear chain would serialise the ALU latencies)
       float mx;
       {
         float t8[8];
@@ -418,14 +432,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int g = 0; g < 8; ++g) {
           float a = fmaxf(s[g], s[g + 8]);
 #pragma unroll
-          for (int c = g + 16; c < 128; c += 16) a = fmaxf(a, fmaxf(s[c], s[c + 8]));
+          for (int c = g + 16; c < CW; c += 16) a = fmaxf(a, fmaxf(s[c], s[c + 8]));
           t8[g] = a;
         }
         mx = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
                    fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
       }
+      if (kSplit == 2) {
+        // both halves must use the same offset: exchange the half-row maxima
+        // as bf16 rounded towards +inf, and both take the max of the two
+        // rounded values (any offset >= the row max is exact for softmax).
+        // The barrier also orders this half's S loads before the partner's P
+        // stores into the upper S columns.
+        const uint16_t mine = __bfloat16_as_ushort(__float2bfloat16_ru(mx));
+        xch[(buf * 2 + h) * 128 + r] = mine;
+        tc::fence_before_sync();  // order the tcgen05.ld above before the partner's st
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + qw) : "memory");
+        tc::fence_after_sync();
+        const uint16_t other = xch[(buf * 2 + (h ^ 1)) * 128 + r];
+        mx = fmaxf(__bfloat162float(__ushort_as_bfloat16(mine)),
+                   __bfloat162float(__ushort_as_bfloat16(other)));
+      }
       const float mxs = mx * scale_log2;
-      // warp-uniform (tcgen05.ld/st are .sync.aligned); always true for n = 0
+      // warp-uniform (tcgen05.ld/st are .sync.aligned); always true for n = 0;
+      // identical in both halves (same rows, same values)
       if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
         const float m_new = fmaxf(m_used, mxs);
         if (n > 0) {
@@ -434,13 +464,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_wait(bar_pv, (n - 1) & 1);  // P V (n-1) has finished writing O
           tc::fence_after_sync();
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t r[32];
-            tc::ld_32x32b_x32(tO + c * 32, r);
+          for (int c = 0; c < DW / 32; ++c) {
+            uint32_t rr[32];
+            tc::ld_32x32b_x32(tO + c * 32, rr);
             tc::wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
-            tc::st_32x32b_x32(tO + c * 32, r);
+            for (int e = 0; e < 32; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * f);
+            tc::st_32x32b_x32(tO + c * 32, rr);
           }
         }
         m_used = m_new;
@@ -450,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 sl2 = make_float2(scale_log2, scale_log2);
       const float2 nm = make_float2(-m_used, -m_used);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -465,7 +495,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc4[e & 3] = add2(acc4[e & 3], pp);
           pk[e] = pack_bf16(pp.x, pp.y);
         }
-        tc::st_32x32b_x16(tS + 64 + c * 16, pk);
+        // P (bf16 pairs) of S columns [32 c', 32 c' + 32) -> TMEM columns 64 + 16 c'
+        tc::st_32x32b_x16(tS + 64 + (h * (CW / 32) + c) * 16, pk);
       }
       const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
       l_sum += acc.x + acc.y;
@@ -484,34 +515,42 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     }
     // epilogue: O / l -> bf16, LSE
-    if (lane == 0) TC_DBG(2 + warp, 9000);
+    if (lane == 0) TC_DBG(2 + (warp & 3), 9000);
+    if (kSplit == 2) {  // l = l_0 + l_1 (the exchange buffers are free after this barrier)
+      float* xl = reinterpret_cast<float*>(smem + C::kOffXch);  // [2][128]
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + qw) : "memory");
+      xl[h * 128 + r] = l_sum;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + qw) : "memory");
+      l_sum = xl[r] + xl[128 + r];
+    }
     tc::mbar_wait(bar_pv, (cnt - 1) & 1);
     tc::fence_after_sync();
-    const int row = i * 128 + warp * 32 + lane;
+    const int row = i * 128 + r;
     const float inv = 1.f / l_sum;
-    __nv_bfloat16* orow = O + (u * N + row) * int64_t(D);
+    __nv_bfloat16* orow = O + (u * N + row) * int64_t(D) + h * DW;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      tc::ld_32x32b_x32(tO + c * 32, r);
+    for (int c = 0; c < DW / 32; ++c) {
+      uint32_t rr[32];
+      tc::ld_32x32b_x32(tO + c * 32, rr);
       tc::wait_ld();
       if (row < N) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           uint4 v;
-          v.x = pack_bf16(__uint_as_float(r[8 * e + 0]) * inv, __uint_as_float(r[8 * e + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv);
+          v.x = pack_bf16(__uint_as_float(rr[8 * e + 0]) * inv, __uint_as_float(rr[8 * e + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(rr[8 * e + 2]) * inv, __uint_as_float(rr[8 * e + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(rr[8 * e + 4]) * inv, __uint_as_float(rr[8 * e + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(rr[8 * e + 6]) * inv, __uint_as_float(rr[8 * e + 7]) * inv);
           *reinterpret_cast<uint4*>(orow + c * 32 + e * 8) = v;
         }
       }
     }
-    if (row < N && LSE) LSE[u * N + row] = (m_used + log2f(l_sum)) * 0.69314718055994531f;
+    if (h == 0 && row < N && LSE)
+      LSE[u * N + row] = (m_used + log2f(l_sum)) * 0.69314718055994531f;
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
   }
