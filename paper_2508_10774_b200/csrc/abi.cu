@@ -106,7 +106,7 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   if (!q || !k || !v || !kv_idx || !kv_cnt || !o) return BLADE_ERR_INVALID_ARG;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
   if (BH < 1 || N < 1 || block < 1 || !(scale > 0.f) || !isfinite(scale)) return BLADE_ERR_INVALID_ARG;
-  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_MMA_SYNC) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_PAIR) return BLADE_ERR_INVALID_ARG;
   if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
@@ -116,8 +116,14 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
     return BLADE_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
+  // AUTO: the two-blocks-per-CTA kernel where it is faster on B200 (d = 64,
+  // Cog layer 1.03 vs 1.13 ms), the one-block kernel for d = 128 (1.19 vs 1.20)
+  const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64);
   if (impl == BLADE_ATTN_MMA_SYNC) {
     e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
+  } else if (pair) {
+    e = blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
+    if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   } else {
     e = blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
                               static_cast<char*>(workspace), workspace_bytes, s);
@@ -152,7 +158,7 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
     return BLADE_ERR_INVALID_ARG;
   if (BH < 1 || N < 1 || block < 1 || window < 1 || !(scale > 0.f) || !isfinite(scale))
     return BLADE_ERR_INVALID_ARG;
-  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_MMA_SYNC) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_PAIR) return BLADE_ERR_INVALID_ARG;
   if (block != kGpuBlock || (d != 64 && d != 128) || impl == BLADE_ATTN_MMA_SYNC)
     return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
@@ -162,9 +168,13 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
   if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return BLADE_ERR_WORKSPACE;
   const blade::GtProblem g{kg, vg, int((int64_t(N) + window - 1) / window), int(window)};
-  cudaError_t e = blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
-                                        static_cast<char*>(workspace), workspace_bytes,
-                                        static_cast<cudaStream_t>(stream), &g);
+  cudaError_t e =
+      (impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64))
+          ? blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse,
+                                   static_cast<cudaStream_t>(stream), &g)
+          : blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
+                                  static_cast<char*>(workspace), workspace_bytes,
+                                  static_cast<cudaStream_t>(stream), &g);
   if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
 }

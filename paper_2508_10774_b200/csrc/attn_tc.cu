@@ -34,10 +34,15 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
+#include "attn_common.cuh"
 #include "tma_host.h"
 
 namespace blade {
 namespace {
+
+using attn::DefaultScale;
+using attn::ex2_poly2;
+using attn::GtArgs;
 
 template <int D>
 struct Cfg {
@@ -100,37 +105,6 @@ constexpr uint32_t kEmuMask = BLADE_ATTN_EMU_MASK;
   } while (0)
 #endif
 
-// 2^x for a pair on the FMA pipe: x = n + f with n = rint(x) (1.5 * 2^23
-// trick), f in [-1/2, 1/2], 2^f by a degree-3 minimax polynomial (|rel err|
-// < 7.5e-5, far below the bf16 rounding P gets next), n added to the exponent
-// field.  Packed fp32x2 ops: 6 FMA-pipe slots for two exponentials.
-BLADE_DEVINL float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 t = add2(x, make_float2(12582912.f, 12582912.f));
-  const float2 n = add2(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = fma2(n, make_float2(-1.f, -1.f), x);
-  float2 p = fma2(f, make_float2(5.517165314e-2f, 5.517165314e-2f),
-                  make_float2(2.426111615e-1f, 2.426111615e-1f));
-  p = fma2(p, f, make_float2(6.932609919e-1f, 6.932609919e-1f));
-  p = fma2(p, f, make_float2(9.999280713e-1f, 9.999280713e-1f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-
-// fp32(1/sqrt(d)) * fp32(log2 e) as the host computes it for the default
-// scale; baking it in lets the exponent FFMA use its immediate form.
-template <int D>
-struct DefaultScale;
-template <>
-struct DefaultScale<128> {
-  static constexpr float kScaleLog2 = 0.088388346f * 1.44269502f;
-};
-template <>
-struct DefaultScale<64> {
-  static constexpr float kScaleLog2 = 0.125f * 1.44269502f;
-};
-
 #ifdef BLADE_ATTN_TRACE  // timing experiment: event timeline of one CTA
 __device__ long long g_tr[8][64];
 #define TR(ev, n, cond)                                                               \
@@ -146,15 +120,6 @@ __device__ long long g_tr[8][64];
 __device__ unsigned long long g_tm[10];
 #define TM_ADD(i, v) atomicAdd(&g_tm[i], (unsigned long long)(v))
 #endif
-
-// Global tokens of ASA_GT: N_g pooled K/V rows attended by every
-// query after its kept blocks, as ceil(N_g/128) extra tiles with the additive
-// bias ln(n_w) (readings R-18..R-20), applied in raw-score units (/ scale).
-struct GtArgs {
-  int Ng;             // number of global tokens (0: plain ASA)
-  float bias_full;    // ln(n) / scale      (full windows)
-  float bias_last;    // ln(n_last) / scale (the last, possibly partial, window)
-};
 
 template <int D, bool kDefaultScale, bool kGT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -249,7 +214,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ahead of the ring: a block's first touch comes from HBM
       for (int n = 0; n < BLADE_ATTN_L2_PREFETCH && n < cnt_fine; ++n)
         for (int p = 0; p < C::kPanels; ++p) tc::tma_prefetch_3d(m, p * 64, list[n] * 128, int(u));
+      int jn = cnt_fine > 0 ? __ldg(list) : 0;  // block id, loaded one item ahead
       for (int n = 0; n < cnt; ++n) {
+        const int jb = jn;
+        if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
         const int s = n % R;
         TC_DBG(0, n);
         if (BLADE_ATTN_L2_PREFETCH > 0 && n + BLADE_ATTN_L2_PREFETCH < cnt_fine)
@@ -274,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_arrive_expect_tx(full + s, C::kTile);
         const bool fine = !kGT || n < cnt_fine;
         const CUtensorMap* mm = fine ? m : (isK ? &tmKg : &tmVg);
-        const int row0 = fine ? list[n] * 128 : (n - cnt_fine) * 128;
+        const int row0 = fine ? jb * 128 : (n - cnt_fine) * 128;
         for (int p = 0; p < C::kPanels; ++p)
           tc::tma_load_3d(dst + p * C::kPanel, mm, full + s, p * 64, row0, int(u));
 #endif
@@ -383,8 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc::mbar_arrive(bar_qt);
     }
     float m_used = -INFINITY, l_sum = 0.f;
+    int jn = cnt_fine > 0 ? __ldg(list) : 0;  // block id, loaded one tile ahead
     for (int n = 0; n < cnt; ++n) {
       const int buf = n & 1;
+      const int jb = jn;
+      if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
       const uint32_t tS = tmem + lane_base + buf * 128;
       if (lane == 0) TC_DBG(2 + (warp & 3), 10 * n + 1);
 #ifdef BLADE_ATTN_TIMING
@@ -413,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const bool fine = !kGT || n < cnt_fine;
       // keys of the (possibly partial) last block / global-token tile
-      const int valid = (fine ? N - list[n] * 128 : gt.Ng - (n - cnt_fine) * 128) - h * CW;
+      const int valid = (fine ? N - jb * 128 : gt.Ng - (n - cnt_fine) * 128) - h * CW;
       if (valid < CW) {
 #pragma unroll
         for (int c = 0; c < CW; ++c)

@@ -95,6 +95,11 @@ cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k,
                            void* o, float* lse, char* ws, size_t ws_bytes,
                            cudaStream_t stream, const GtProblem* gt = nullptr);
 
+// Two query blocks per CTA (ping-pong softmax warpgroups), attn_tc2.cu.
+cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, const void* v,
+                            const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
+                            cudaStream_t stream, const GtProblem* gt = nullptr);
+
 // MeanPool_n of K and V, fp32 accumulation, bf16 round-to-nearest.
 cudaError_t launch_gt_pool(const void* k, const void* v, int64_t BH, int N, int d, int window,
                            void* kg, void* vg, cudaStream_t stream);

@@ -67,8 +67,9 @@ GT_CASES = [  # (BH, N, d, window, density)
 ]
 
 
+@pytest.mark.parametrize("impl", [1, 3], ids=["tcgen05", "pair"])
 @pytest.mark.parametrize("case", GT_CASES, ids=lambda c: "x".join(map(str, c)))
-def test_gt_attention_parity_given_mask(A, case):
+def test_gt_attention_parity_given_mask(A, case, impl):
     BH, N, d, n, density = case
     q, k, v = inputs.iid(1, BH, N, d, seed=N + d + n)
     Nb = O.num_blocks(N, 128)
@@ -77,7 +78,7 @@ def test_gt_attention_parity_given_mask(A, case):
     qd, kd, vd = PT.to_dev(q, k, v)
     ki, kc = PT.lists_to_dev(kv_idx, kv_cnt)
     kg, vg = A.blade_gt_pool(kd, vd, window=n)
-    o, lse = A.blade_bsa_gt_fwd(qd, kd, vd, ki, kc, kg, vg, window=n)
+    o, lse = A.blade_bsa_gt_fwd(qd, kd, vd, ki, kc, kg, vg, window=n, impl=impl)
     torch.cuda.synchronize()
     PT.check_attention(o, lse, o_ref, lse_ref)
 

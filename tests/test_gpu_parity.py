@@ -22,7 +22,7 @@ def A(cuda_dev):
     return asa
 
 
-IMPLS = [pytest.param(2, id="mma_sync"), pytest.param(1, id="tcgen05")]
+IMPLS = [pytest.param(2, id="mma_sync"), pytest.param(1, id="tcgen05"), pytest.param(3, id="pair")]
 
 
 def _run_mask(A, q, k, p: O.AsaParams, **kw):
