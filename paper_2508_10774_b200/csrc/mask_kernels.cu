@@ -347,6 +347,117 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(
 // ---------------------------------------------------------------------------
 constexpr int RF_THREADS = 128;
 
+#ifdef BLADE_RF_TIMING  // timing experiment: globaltimer stamps (ns) of the refine phases
+__device__ unsigned long long g_rf[8];  // 0 min start, 1 max end, 2 max item end, 3 sum combine,
+                                        // 4 sum select, 5 rows, 6 max item duration
+BLADE_DEVINL unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+// Alg. 1 l.7-10 for one refined row by the whole CTA, in fp64:
+// Z = sum_j P_imp (block reduction), p~_j = P_imp_j / Z (l.7); the rank of
+// each p~_j in the order (p~ desc, id asc) (l.8, reading R-7) by counting, so
+// the selection order is the oracle's exactly; C_m by a block scan of the
+// sorted values, m0 = first m with C_m >= tau (N_b if none or tau >= 1,
+// reading R-4), m = clamp(m0, lo, hi) (l.9); kept = rank < m, compacted in
+// ascending id order (l.10).  Summation orders differ from the oracle's
+// sequential sums only by fp64 rounding (~1e-16), far inside the 1e-6 tie band.
+template <int NT>
+__device__ void refine_select_cta(double* p, double* sorted, int* rank, double* scan, int* cnt,
+                                  int Nb, double tau, int lo, int hi, uint8_t* mask_row,
+                                  int32_t* kv_idx_row, int32_t* kv_cnt_out) {
+  const int tid = threadIdx.x;
+  constexpr int PER = kMaxNb / NT;  // items per thread (Nb <= kMaxNb)
+  // Z
+  double z = 0.0;
+  for (int j = tid; j < Nb; j += NT) z += p[j];
+  scan[tid] = z;
+  __syncthreads();
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    if (tid < o) scan[tid] += scan[tid + o];
+    __syncthreads();
+  }
+  const double Z = scan[0];
+  __syncthreads();
+  for (int j = tid; j < Nb; j += NT) p[j] = p[j] / Z;
+  __syncthreads();
+  // ranks and the sorted row
+  for (int j = tid; j < Nb; j += NT) {
+    const double v = p[j];
+    int r = 0;
+    for (int k = 0; k < Nb; ++k) {
+      const double w = p[k];
+      r += (w > v || (w == v && k < j)) ? 1 : 0;
+    }
+    rank[j] = r;
+    sorted[r] = v;
+  }
+  __syncthreads();
+  // C_m: thread t owns sorted positions [t PER, (t+1) PER)
+  double c[PER];
+  double run = 0.0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int x = tid * PER + e;
+    run += x < Nb ? sorted[x] : 0.0;
+    c[e] = run;
+  }
+  scan[tid] = run;
+  __syncthreads();
+  for (int o = 1; o < NT; o <<= 1) {  // inclusive Hillis-Steele scan of the thread totals
+    const double add = tid >= o ? scan[tid - o] : 0.0;
+    __syncthreads();
+    scan[tid] += add;
+    __syncthreads();
+  }
+  const double base = tid > 0 ? scan[tid - 1] : 0.0;
+  int first = Nb + 1;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int x = tid * PER + e;
+    if (x < Nb && base + c[e] >= tau && first > Nb) first = x + 1;
+  }
+  cnt[tid] = first;
+  __syncthreads();
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    if (tid < o) cnt[tid] = min(cnt[tid], cnt[tid + o]);
+    __syncthreads();
+  }
+  const int m0 = (tau >= 1.0 || cnt[0] > Nb) ? Nb : cnt[0];
+  const int m = min(max(m0, lo), hi);
+  __syncthreads();
+  // l.10: kept = rank < m, ascending ids: block-contiguous ranges of j per thread
+  int kept_here = 0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int j = tid * PER + e;
+    if (j < Nb && rank[j] < m) ++kept_here;
+  }
+  cnt[tid] = kept_here;
+  __syncthreads();
+  for (int o = 1; o < NT; o <<= 1) {
+    const int add = tid >= o ? cnt[tid - o] : 0;
+    __syncthreads();
+    cnt[tid] += add;
+    __syncthreads();
+  }
+  int pos = cnt[tid] - kept_here;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int j = tid * PER + e;
+    if (j < Nb) {
+      const bool keep = rank[j] < m;
+      if (mask_row) mask_row[j] = keep ? 1 : 0;
+      if (keep) kv_idx_row[pos++] = j;
+    }
+  }
+  for (int x = m + tid; x < Nb; x += NT) kv_idx_row[x] = -1;
+  if (tid == 0) *kv_cnt_out = m;
+}
+
 // CK = sampled keys per work item (64 for k <= 64, 128 for k = 128): a thread
 // owns one key and RPT = 16 CK / 128 of the block's (up to 16) query rows.
 template <int D, int CK>
@@ -364,16 +475,26 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
   __shared__ double sRg[8][16];                // [16-key group][s] group max
   __shared__ double sW[4][16];                 // per-warp partials
   __shared__ double sMc[16];
-  __shared__ float sRow[kMaxNb];
-  __shared__ double sMs[128], sLs[128];
-  __shared__ uint32_t keep_bits[16];
+  __shared__ double sRow[kMaxNb];     // refined P_imp row, then p~ (l.7)
+  __shared__ double sSorted[kMaxNb];  // p~ in selection order (l.8)
+  __shared__ int sRank[kMaxNb];
+  __shared__ double sMs[128];
+  __shared__ double sScan[RF_THREADS];
+  __shared__ int sCnt[RF_THREADS];
   __shared__ int last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kt = tid % CK, hr = tid / CK;
   const int nflag = counters[0];
   if (blockIdx.x == 0 && tid == 0 && n_refined) *n_refined = nflag;
   const int NK = Nb * kk;
+#ifdef BLADE_RF_TIMING
+  const unsigned long long t_cta = gtime();
+  if (tid == 0) atomicMin(&g_rf[0], t_cta);
+#endif
   for (int item = blockIdx.x; item < nflag * nchunks; item += gridDim.x) {
+#ifdef BLADE_RF_TIMING
+    const unsigned long long t_item = gtime();
+#endif
     const int f = item / nchunks, c = item % nchunks;
     const int64_t row = flags[f];
     const int64_t u = row / Nb;
@@ -463,56 +584,102 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
       }
     }
     // ---- last chunk of this row: combine and reselect ----
+#ifdef BLADE_RF_TIMING
+    if (tid == 0) {
+      const unsigned long long te = gtime();
+      atomicMax(&g_rf[2], te);
+      atomicMax(&g_rf[6], te - t_item);
+    }
+    const unsigned long long t_comb = gtime();
+#endif
     __threadfence();
     __syncthreads();
     if (tid == 0) last = (atomicAdd(&done[f], 1) == nchunks - 1);
     __syncthreads();
     if (!last) continue;
     __threadfence();
-    // l.14 combine, spread over all threads: (query row q, chunk stripe z)
-    {
-      const int q = tid & 15, z = tid >> 4;  // 16 rows x 8 stripes
+    // l.14 combine, spread over all threads: (query row q, chunk stripe z);
+    // each thread issues all of its loads before using any (one L2 latency)
+    for (int qg = 0; qg < ki; qg += 16) {  // query rows in groups of 16
+      const int q = qg + (tid & 15), z = tid >> 4;  // 16 rows x 8 stripes
+      constexpr int kMaxPer = 16;            // loads in flight per thread and pass
       double M = -INFINITY;
-      if (q < ki)
-        for (int cc = z; cc < nchunks; cc += 8)
-          M = fmax(M, __ldcg(&mpart[(int64_t(f) * nchunks + cc) * kk + q]));
-      sRg[z][q] = M;
-      __syncthreads();
-      M = sRg[0][q];
+      for (int b0 = 0; b0 < nchunks; b0 += 8 * kMaxPer) {
+        double mv[kMaxPer];
 #pragma unroll
-      for (int zz = 1; zz < 8; ++zz) M = fmax(M, sRg[zz][q]);
-      double l = 0.0;
-      if (q < ki)
-        for (int cc = z; cc < nchunks; cc += 8) {
-          const int64_t o = (int64_t(f) * nchunks + cc) * kk + q;
-          const double mc = __ldcg(&mpart[o]);
-          if (mc != -INFINITY) l += __ldcg(&lpart[o]) * exp(mc - M);
+        for (int e = 0; e < kMaxPer; ++e) {
+          const int cc = b0 + z + 8 * e;
+          const bool ok = q < ki && cc < nchunks;
+          mv[e] = ok ? __ldcg(&mpart[(int64_t(f) * nchunks + cc) * kk + q]) : -INFINITY;
         }
+#pragma unroll
+        for (int e = 0; e < kMaxPer; ++e) M = fmax(M, mv[e]);
+      }
+      sRg[z][q - qg] = M;
       __syncthreads();
-      sRg[z][q] = l;
+      M = sRg[0][q - qg];
+#pragma unroll
+      for (int zz = 1; zz < 8; ++zz) M = fmax(M, sRg[zz][q - qg]);
+      double l = 0.0;
+      for (int b0 = 0; b0 < nchunks; b0 += 8 * kMaxPer) {
+        double mv[kMaxPer], lv[kMaxPer];
+#pragma unroll
+        for (int e = 0; e < kMaxPer; ++e) {
+          const int cc = b0 + z + 8 * e;
+          const bool ok = q < ki && cc < nchunks;
+          const int64_t o = (int64_t(f) * nchunks + (ok ? cc : 0)) * kk + (ok ? q : 0);
+          mv[e] = ok ? __ldcg(&mpart[o]) : -INFINITY;
+          lv[e] = ok ? __ldcg(&lpart[o]) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < kMaxPer; ++e)
+          if (mv[e] != -INFINITY) l += lv[e] * exp(mv[e] - M);
+      }
+      __syncthreads();
+      sRg[z][q - qg] = l;
       __syncthreads();
       if (z == 0 && q < ki) {
         double lt = 0.0;
 #pragma unroll
-        for (int zz = 0; zz < 8; ++zz) lt += sRg[zz][q];
+        for (int zz = 0; zz < 8; ++zz) lt += sRg[zz][q - qg];
         sMs[q] = M + log(lt);  // P~ = e^{L - M} / l = e^{L - (M + ln l)}
       }
+      __syncthreads();
     }
-    __syncthreads();
     // l.17-19: P_imp[j] = max_s e^{R_sj - M_s} / l_s = e^{max_s (R_sj - M_s - ln l_s)}
     for (int j = tid; j < Nb; j += RF_THREADS) {
+      double rv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        rv[q] = q < ki ? __ldcg(&r64[(int64_t(f) * kk + q) * Nb + j]) : -INFINITY;
       double arg = -INFINITY;
-      for (int q = 0; q < ki; ++q)
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < ki) arg = fmax(arg, rv[q] - sMs[q]);
+      for (int q = 16; q < ki; ++q)  // k > 16 only
         arg = fmax(arg, __ldcg(&r64[(int64_t(f) * kk + q) * Nb + j]) - sMs[q]);
       const double best = exp(arg);
-      sRow[j] = float(best);
+      sRow[j] = best;
       if (pimp_out) pimp_out[row * Nb + j] = float(best);
     }
     __syncthreads();
-    if (warp == 0)
-      select_row(static_cast<const float*>(sRow), Nb, tau, lo, hi, 0.0, false,
-                 mask ? mask + row * Nb : nullptr, kv_idx + row * Nb, kv_cnt + row, keep_bits);
+#ifdef BLADE_RF_TIMING
+    const unsigned long long t_sel = gtime();
+#endif
+    refine_select_cta<RF_THREADS>(sRow, sSorted, sRank, sScan, sCnt, Nb, tau, lo, hi,
+                      mask ? mask + row * Nb : nullptr, kv_idx + row * Nb, kv_cnt + row);
+#ifdef BLADE_RF_TIMING
+    if (tid == 0) {
+      const unsigned long long t_done = gtime();
+      atomicAdd(&g_rf[3], t_sel - t_comb);
+      atomicAdd(&g_rf[4], t_done - t_sel);
+      atomicAdd(&g_rf[5], 1ull);
+    }
+#endif
   }
+#ifdef BLADE_RF_TIMING
+  if (tid == 0) atomicMax(&g_rf[1], gtime());
+#endif
 }
 
 template <int D>
@@ -573,6 +740,19 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     refine_kernel<D, 128><<<148 * 3, RF_THREADS, 0, stream>>>(
         qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
         flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
+#ifdef BLADE_RF_TIMING
+  {
+    static int calls = 0;
+    unsigned long long h[8], z[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h, g_rf, sizeof(h));
+    cudaMemcpyToSymbol(g_rf, z, sizeof(z));
+    if (++calls % 10 == 0 && h[5])
+      fprintf(stderr, "refine: kernel %.1f us, items end at %.1f us (max item %.1f us), %llu rows: "
+              "combine %.1f us, select %.1f us per row\n", (h[1] - h[0]) * 1e-3,
+              (h[2] - h[0]) * 1e-3, h[6] * 1e-3, h[5], h[3] * 1e-3 / h[5], h[4] * 1e-3 / h[5]);
+  }
+#endif
   return cudaGetLastError();
 }
 

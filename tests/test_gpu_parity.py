@@ -152,3 +152,32 @@ def test_invariants_ones_and_determinism(A, impl):
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2) and torch.equal(m1.kv_idx, m2.kv_idx)
     assert (o1.float() - 1).abs().max().item() <= 4e-3          # V = 1 => O = 1
+
+
+REFINE_CASES = [
+    # (H, N, d, samples, recipe, tau) -- every row forced through the fp64 refinement
+    (2, 1000, 128, 16, "smooth", 0.9),
+    (2, 777, 64, 16, "iid", 0.8),
+    (1, 2000, 64, 32, "smooth", 0.95),
+    (1, 1500, 128, 64, "iid", 0.7),
+    (1, 700, 64, 128, "smooth", 0.9),
+    (1, 70, 128, 16, "iid", 0.5),
+]
+
+
+@pytest.mark.parametrize("case", REFINE_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_refine_path_every_row(A, case):
+    """refine_guard = 1e30 flags every row: the fp64 recomputation (K-mask.4)
+    and its CTA-wide reselection must reproduce the oracle's mask (bit-exact
+    outside the tie band) and its fp64 P_imp (to the fp32 rounding of the
+    output)."""
+    H, N, d, kk, recipe, tau = case
+    q, k, _ = _inputs(1, H, N, d, recipe)
+    p = O.AsaParams(tau=tau, samples=kk)
+    ref = O.asa_mask(q, k, p)
+    got = _run_mask(A, q, k, p, refine_guard=1e30)
+    torch.cuda.synchronize()
+    Nb = O.num_blocks(N, 128)
+    assert int(got.n_refined.item()) >= H * Nb - H  # rows with m = N_b may skip (T2 needs m < N_b)
+    PT.check_mask(ref, got, p)
+    np.testing.assert_allclose(got.p_imp.cpu().numpy(), ref.p_imp, rtol=1e-7, atol=0)
