@@ -565,3 +565,92 @@ def sparse_attention_gt(q, k, v, kv_idx, kv_cnt, b: int, n: int, scale: float | 
         O[u], LSE[u] = sparse_attention_gt_unit(q[u], k[u], v[u], kv_idx[u], kv_cnt[u], b,
                                                 scale, n, qblocks)
     return O, LSE
+
+
+# ---------------------------------------------------------------------------
+# F2  locality-preserving token rearrangement ("we employ a Gilbert
+#     space-filling curve to reorder the tokens before blocking"; Alg. 1 l.1
+#     P:143 "Rearrange tokens using Gilbert curve").  Readings:
+#       R-21  the paper does not say 2-D or 3-D: each frame's h x w patch grid
+#             is ordered by the 2-D generalised Hilbert ("Gilbert") curve,
+#             frames stay in temporal order (frame-major), so every 128-token
+#             block is a compact patch of one frame and the curve keeps exact
+#             4-neighbour adjacency inside a frame;
+#       R-22  leading text tokens (CogVideoX) keep their positions.
+#     The curve is the recursive construction for arbitrary rectangles: split
+#     the long side in two when the rectangle is more than 1.5x longer than
+#     wide, else cut it into three parts (one step along the short side, the
+#     long run, one step back), halves rounded so the sub-rectangles' major
+#     sides are even where possible, which is what keeps consecutive cells
+#     adjacent.
+# ---------------------------------------------------------------------------
+
+
+def _sgn(x: int) -> int:
+    return (x > 0) - (x < 0)
+
+
+def gilbert2d_cells(width: int, height: int) -> list:
+    """(x, y) cells of a width x height grid in Gilbert-curve order, starting
+    at (0, 0) and running along the longer side."""
+    out = []
+
+    def walk(x, y, ax, ay, bx, by):
+        w, h = abs(ax + ay), abs(bx + by)
+        dax, day, dbx, dby = _sgn(ax), _sgn(ay), _sgn(bx), _sgn(by)
+        if h == 1:                      # a single row: walk it
+            for _ in range(w):
+                out.append((x, y))
+                x, y = x + dax, y + day
+            return
+        if w == 1:                      # a single column
+            for _ in range(h):
+                out.append((x, y))
+                x, y = x + dbx, y + dby
+            return
+        ax2, ay2, bx2, by2 = ax // 2, ay // 2, bx // 2, by // 2
+        w2, h2 = abs(ax2 + ay2), abs(bx2 + by2)
+        if 2 * w > 3 * h:               # long rectangle: two halves along the major axis
+            if (w2 % 2) and (w > 2):
+                ax2, ay2 = ax2 + dax, ay2 + day
+            walk(x, y, ax2, ay2, bx, by)
+            walk(x + ax2, y + ay2, ax - ax2, ay - ay2, bx, by)
+        else:                           # up, across, down
+            if (h2 % 2) and (h > 2):
+                bx2, by2 = bx2 + dbx, by2 + dby
+            walk(x, y, bx2, by2, ax2, ay2)
+            walk(x + bx2, y + by2, ax, ay, bx - bx2, by - by2)
+            walk(x + (ax - dax) + (bx2 - dbx), y + (ay - day) + (by2 - dby),
+                 -bx2, -by2, -(ax - ax2), -(ay - ay2))
+
+    if width >= height:                 # major axis x (length width), minor y
+        walk(0, 0, width, 0, 0, height)
+    else:                               # major axis y (length height), minor x
+        walk(0, 0, 0, height, width, 0)
+    return out
+
+
+def gilbert_permutation(t: int, h: int, w: int, n_text: int = 0) -> np.ndarray:
+    """perm[i] = raster index (text tokens first, then t-major, y, x) of the
+    token placed at position i of the rearranged sequence (R-21, R-22)."""
+    if min(t, h, w) < 1 or n_text < 0:
+        raise ValueError("grid extents must be positive")
+    cells = gilbert2d_cells(w, h)       # (x, y) along the frame
+    frame = np.array([y * w + x for x, y in cells], dtype=np.int64)
+    perm = [np.arange(n_text, dtype=np.int64)]
+    for f in range(t):
+        perm.append(n_text + f * h * w + frame)
+    return np.concatenate(perm)
+
+
+def apply_permutation(x, perm: np.ndarray) -> np.ndarray:
+    """x'[.., i, :] = x[.., perm[i], :] (token axis = -2)."""
+    return np.asarray(x)[..., perm, :]
+
+
+def undo_permutation(x, perm: np.ndarray) -> np.ndarray:
+    """Inverse of apply_permutation: y[.., perm[i], :] = x[.., i, :]."""
+    x = np.asarray(x)
+    y = np.empty_like(x)
+    y[..., perm, :] = x
+    return y
