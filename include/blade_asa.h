@@ -162,6 +162,33 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
                                 int32_t impl, void* workspace, size_t workspace_bytes,
                                 void* stream);
 
+/*
+ * Locality-preserving token rearrangement ("Gilbert space-filling
+ * curve to reorder the tokens before blocking"; Alg. 1 l.1; readings
+ * R-21/R-22): video tokens of a t x h x w latent grid (raster order, after
+ * n_text leading text tokens) are reordered frame by frame along the 2-D
+ * generalised Hilbert curve of each h x w frame; text tokens stay in place.
+ *
+ * blade_gilbert_order — HOST function (no GPU work).
+ *   perm        HOST int32 out, perm_len = n_text + t*h*w entries:
+ *               perm[i] = raster index of the token placed at position i.
+ * Errors: INVALID_ARG (NULL, non-positive extent, n_text < 0, wrong length).
+ */
+blade_status_t blade_gilbert_order(int32_t t, int32_t h, int32_t w, int32_t n_text,
+                                   int32_t* perm, int64_t perm_len);
+
+/*
+ * blade_permute_tokens — DEVICE gather along the token axis of [BH, N, d]
+ * bf16: inverse = 0: out[u, i, :] = x[u, perm[i], :]  (apply the order);
+ *       inverse = 1: out[u, perm[i], :] = x[u, i, :]  (undo it).
+ *   perm        DEVICE int32 [N], a permutation of [0, N) (not checked).
+ *   x, out      distinct, 16-byte aligned; d a multiple of 8.
+ * Errors: INVALID_ARG, CUDA.
+ */
+blade_status_t blade_permute_tokens(const void* x, int64_t BH, int32_t N, int32_t d,
+                                    const int32_t* perm, int32_t inverse, void* out,
+                                    void* stream);
+
 /* Bytes of DEVICE scratch blade_asa_fwd_host needs (0 on bad args / GPU limits). */
 size_t blade_asa_fwd_host_workspace_size(int64_t BH, int32_t N, int32_t d,
                                          const blade_asa_params_t* params,

@@ -31,6 +31,7 @@ ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC, ATTN_TCGEN05_PAIR = 0, 1, 2, 3
 
 ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd_workspace_size",
                "blade_bsa_fwd", "blade_gt_pool", "blade_bsa_gt_fwd",
+               "blade_gilbert_order", "blade_permute_tokens",
                "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
                "blade_status_string", "blade_version")
 
@@ -62,6 +63,10 @@ _lib.blade_gt_pool.argtypes = [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]
 _lib.blade_bsa_gt_fwd.restype = ctypes.c_int
 _lib.blade_bsa_gt_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp,
                                   _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_gilbert_order.restype = ctypes.c_int
+_lib.blade_gilbert_order.argtypes = [_i32, _i32, _i32, _i32, _vp, _i64]
+_lib.blade_permute_tokens.restype = ctypes.c_int
+_lib.blade_permute_tokens.argtypes = [_vp, _i64, _i32, _i32, _vp, _i32, _vp, _vp]
 _lib.blade_asa_fwd_host_workspace_size.restype = _sz
 _lib.blade_asa_fwd_host_workspace_size.argtypes = [_i64, _i32, _i32,
                                                    ctypes.POINTER(BladeAsaParams), _i32]
@@ -290,6 +295,33 @@ def asa_gt_forward(q, k, v, *, window: int = 128, tau: float = 0.9, keep_min: in
                        seed=seed, unit_offset=unit_offset, stream=stream, **mask_kw)
     o, lse = blade_bsa_gt_fwd(q, k, v, m.kv_idx, m.kv_cnt, kg, vg, window=window, stream=stream)
     return o, lse, m
+
+
+def gilbert_order(t: int, h: int, w: int, n_text: int = 0) -> torch.Tensor:
+    """The Gilbert token order (blade_gilbert_order, computed on the host):
+    int32 CPU tensor perm with perm[i] = raster index of the i-th token."""
+    n = n_text + t * h * w
+    perm = torch.empty(n, dtype=torch.int32)
+    st = _lib.blade_gilbert_order(t, h, w, n_text, _ptr(perm), n)
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_gilbert_order")
+    return perm
+
+
+def blade_permute_tokens(x: torch.Tensor, perm: torch.Tensor, *, inverse: bool = False,
+                         out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Token-axis gather on the GPU: x[:, perm] (apply) or its inverse (undo)."""
+    x = _as_units(x, "x")
+    BH, N, d = x.shape
+    if perm.dtype != torch.int32 or not perm.is_cuda or perm.numel() != N:
+        raise ValueError("perm must be a CUDA int32 tensor of N entries")
+    if out is None:
+        out = torch.empty_like(x)
+    st = _lib.blade_permute_tokens(_ptr(x), BH, N, d, _ptr(perm.contiguous()), int(inverse),
+                                   _ptr(out), _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_permute_tokens")
+    return out
 
 
 def _as_host_units(x: torch.Tensor, name: str) -> torch.Tensor:

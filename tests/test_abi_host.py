@@ -160,3 +160,30 @@ def test_gt_validation_codes(asa):
     assert call(impl=A.ATTN_MMA_SYNC) == A.BLADE_ERR_UNSUPPORTED
     assert call(d=256) == A.BLADE_ERR_UNSUPPORTED
     assert call(ws=None) == A.BLADE_ERR_WORKSPACE
+
+
+@pytest.mark.parametrize("t,h,w,n_text", [(1, 16, 32, 0), (21, 30, 52, 0), (13, 30, 45, 226),
+                                          (1, 4, 5, 0), (2, 7, 3, 2), (1, 1, 1, 0), (3, 9, 9, 0)])
+def test_gilbert_order_host_matches_oracle(asa, t, h, w, n_text):
+    """blade_gilbert_order is a host function: compare it with the oracle here."""
+    from oracle import asa_oracle as O
+    perm = asa.gilbert_order(t, h, w, n_text).numpy()
+    assert (perm == O.gilbert_permutation(t, h, w, n_text)).all()
+
+
+def test_gilbert_exhaustive_small_grids_match_oracle(asa):
+    from oracle import asa_oracle as O
+    for h in range(1, 20):
+        for w in range(1, 20):
+            assert (asa.gilbert_order(1, h, w).numpy() == O.gilbert_permutation(1, h, w)).all(), (h, w)
+
+
+def test_gilbert_and_permute_validation(asa):
+    A, lib = asa, asa._lib
+    buf = (ctypes.c_int32 * 8)()
+    assert lib.blade_gilbert_order(1, 2, 4, 0, buf, 7) == A.BLADE_ERR_INVALID_ARG
+    assert lib.blade_gilbert_order(0, 2, 4, 0, buf, 0) == A.BLADE_ERR_INVALID_ARG
+    assert lib.blade_gilbert_order(1, 2, 4, 0, None, 8) == A.BLADE_ERR_INVALID_ARG
+    P = 1 << 20
+    assert lib.blade_permute_tokens(P, 1, 16, 12, P, 0, P + 4096, None) == A.BLADE_ERR_INVALID_ARG
+    assert lib.blade_permute_tokens(P, 1, 16, 64, P, 0, P, None) == A.BLADE_ERR_INVALID_ARG
