@@ -654,3 +654,57 @@ def undo_permutation(x, perm: np.ndarray) -> np.ndarray:
     y = np.empty_like(x)
     y[..., perm, :] = x
     return y
+
+
+# ---------------------------------------------------------------------------
+# F3  block-sparse attention backward (the student "generates its
+#     trajectory using the ASA mechanism" and the loss "updates the student's
+#     weights ... given these dynamic sparsity constraints", so gradients flow
+#     through the masked attention of A9).  The vector-Jacobian product of
+#     O = softmax_T(scale Q K^T) V restricted to the kept blocks T(r):
+#       P_rt  = exp(scale q_r.k_t - LSE_r)             t in T(r), else 0
+#       dV_t  = sum_r P_rt dO_r
+#       dP_rt = dO_r . v_t
+#       D_r   = sum_t P_rt dP_rt  (= dO_r . O_r)
+#       dS_rt = P_rt (dP_rt - D_r)
+#       dQ_r  = scale sum_t dS_rt k_t,   dK_t = scale sum_r dS_rt q_r
+#     The mask M is a constant of the backward (Alg. 1's selection is not
+#     differentiated; reading R-23).
+# ---------------------------------------------------------------------------
+
+
+def sparse_attention_backward_unit(q_u, k_u, v_u, do_u, kv_idx_u, kv_cnt_u, b: int,
+                                   scale: float):
+    """fp64 (dQ, dK, dV) of one unit, query block by query block."""
+    q_u, k_u, v_u, do_u = to_f64(q_u), to_f64(k_u), to_f64(v_u), to_f64(do_u)
+    N, d = q_u.shape
+    Nb = num_blocks(N, b)
+    dq, dk, dv = np.zeros_like(q_u), np.zeros_like(k_u), np.zeros_like(v_u)
+    for i in range(Nb):
+        r0, r1 = i * b, min((i + 1) * b, N)
+        cols = np.concatenate([np.arange(j * b, min((j + 1) * b, N))
+                               for j in kv_idx_u[i, :kv_cnt_u[i]]])
+        S = (q_u[r0:r1] @ k_u[cols].T) * scale
+        mx = S.max(axis=1, keepdims=True)
+        E = np.exp(S - mx)
+        P = E / E.sum(axis=1, keepdims=True)
+        dO = do_u[r0:r1]
+        dv[cols] += P.T @ dO
+        dP = dO @ v_u[cols].T
+        Dr = (P * dP).sum(axis=1, keepdims=True)
+        dS = P * (dP - Dr)
+        dq[r0:r1] += scale * (dS @ k_u[cols])
+        dk[cols] += scale * (dS.T @ q_u[r0:r1])
+    return dq, dk, dv
+
+
+def sparse_attention_backward(q, k, v, do, kv_idx, kv_cnt, b: int, scale: float | None = None,
+                              units=None):
+    """F3 for [BH, N, d]: fp64 dQ, dK, dV (units not listed are NaN)."""
+    q, k, v, do = to_f64(q), to_f64(k), to_f64(v), to_f64(do)
+    scale = default_scale(q.shape[2]) if scale is None else float(scale)
+    dq, dk, dv = (np.full(q.shape, np.nan) for _ in range(3))
+    for u in (range(q.shape[0]) if units is None else units):
+        dq[u], dk[u], dv[u] = sparse_attention_backward_unit(q[u], k[u], v[u], do[u], kv_idx[u],
+                                                             kv_cnt[u], b, scale)
+    return dq, dk, dv
