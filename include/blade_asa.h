@@ -129,6 +129,31 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
                              void* o, float* lse, int32_t impl,
                              void* workspace, size_t workspace_bytes, void* stream);
 
+/* Bytes of scratch blade_bsa_bwd needs (0 on bad args / GPU limits). */
+size_t blade_bsa_bwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block);
+
+/*
+ * blade_bsa_bwd — gradients of blade_bsa_fwd (sparsity-aware
+ * distillation trains through ASA; reading R-23: the kept-block lists are
+ * constants).  With P_rt = exp(scale q_r.k_t - LSE_r) over r's kept keys:
+ *   D_r = dO_r . O_r,  dV_t = sum_r P_rt dO_r,
+ *   dK_t = scale sum_r P_rt (dO_r . v_t - D_r) q_r,
+ *   dQ_r = scale sum_t P_rt (dO_r . v_t - D_r) k_t.
+ *   q, k, v, o, dout   [BH, N, d] bf16 device (o = the forward's O), 16-B aligned.
+ *   lse                [BH, N] fp32 device (the forward's LSE).
+ *   kv_idx, kv_cnt     the forward's lists.
+ *   dq, dk, dv         [BH, N, d] bf16 device out (every row written; key rows
+ *                      no query keeps get 0).
+ *   workspace          >= blade_bsa_bwd_workspace_size() (D_r and the
+ *                      transposed lists).  BH <= 65535.
+ * Deterministic (no atomics).  Errors: INVALID_ARG, UNSUPPORTED, WORKSPACE, CUDA.
+ */
+blade_status_t blade_bsa_bwd(const void* q, const void* k, const void* v, const void* o,
+                             const float* lse, const void* dout, int64_t BH, int32_t N,
+                             int32_t d, int32_t block, float scale, const int32_t* kv_idx,
+                             const int32_t* kv_cnt, void* dq, void* dk, void* dv,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
 /*
  * ASA with global tokens, ASA_GT (Step 2.2 (2); readings R-18..R-20):
  * K_aug = Concat(K, MeanPool_n(K)), V_aug likewise.  Window w of the token

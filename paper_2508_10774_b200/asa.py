@@ -30,7 +30,8 @@ BLADE_OK, BLADE_ERR_INVALID_ARG, BLADE_ERR_UNSUPPORTED, BLADE_ERR_WORKSPACE, BLA
 ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC, ATTN_TCGEN05_PAIR = 0, 1, 2, 3
 
 ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd_workspace_size",
-               "blade_bsa_fwd", "blade_gt_pool", "blade_bsa_gt_fwd",
+               "blade_bsa_fwd", "blade_bsa_bwd_workspace_size", "blade_bsa_bwd",
+               "blade_gt_pool", "blade_bsa_gt_fwd",
                "blade_gilbert_order", "blade_permute_tokens",
                "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
                "blade_status_string", "blade_version")
@@ -58,6 +59,11 @@ _lib.blade_bsa_fwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
 _lib.blade_bsa_fwd.restype = ctypes.c_int
 _lib.blade_bsa_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp, _vp,
                                _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_bsa_bwd_workspace_size.restype = _sz
+_lib.blade_bsa_bwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
+_lib.blade_bsa_bwd.restype = ctypes.c_int
+_lib.blade_bsa_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32,
+                               ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.blade_gt_pool.restype = ctypes.c_int
 _lib.blade_gt_pool.argtypes = [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]
 _lib.blade_bsa_gt_fwd.restype = ctypes.c_int
@@ -229,6 +235,30 @@ def blade_bsa_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_idx: tor
     if st != BLADE_OK:
         raise BladeError(st, "blade_bsa_fwd")
     return o, lse
+
+
+def blade_bsa_bwd(q, k, v, o, lse, do, kv_idx, kv_cnt, *, scale: float | None = None,
+                  block: int = 128, dq=None, dk=None, dv=None, stream=None):
+    """Gradients of the block-sparse attention -> (dQ, dK, dV) bf16."""
+    q, k, v, o, do = (_as_units(x, n) for x, n in ((q, "q"), (k, "k"), (v, "v"), (o, "o"),
+                                                    (do, "do")))
+    BH, N, d = q.shape
+    if lse.dtype != torch.float32 or not lse.is_cuda or tuple(lse.shape) != (BH, N):
+        raise ValueError("lse must be CUDA fp32 [BH, N]")
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    nbytes = _lib.blade_bsa_bwd_workspace_size(BH, N, d, block)
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_bwd_workspace_size")
+    ws = _workspace(nbytes, q.device, "bwd")
+    st = _lib.blade_bsa_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse.contiguous()), _ptr(do),
+                            BH, N, d, block, default_scale(d) if scale is None else scale,
+                            _ptr(kv_idx), _ptr(kv_cnt), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws),
+                            ws.numel(), _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_bsa_bwd")
+    return dq, dk, dv
 
 
 def num_global_tokens(N: int, window: int) -> int:

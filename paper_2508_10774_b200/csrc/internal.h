@@ -100,6 +100,25 @@ cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, 
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
                             cudaStream_t stream, const GtProblem* gt = nullptr);
 
+// Block-sparse attention backward (attn_bwd.cu): workspace = D_r (fp32
+// [BH, N]) + transposed lists q_idx [BH, N_b, N_b] + q_cnt [BH, N_b].
+struct BwdWorkspace {
+  size_t off_d, off_qidx, off_qcnt, total;
+};
+inline BwdWorkspace bwd_workspace_layout(const AttnProblem& p) {
+  BwdWorkspace w{};
+  size_t o = 0;
+  w.off_d = o;    o = align256(o + size_t(p.BH) * p.N * 4);
+  w.off_qidx = o; o = align256(o + size_t(p.BH) * p.Nb * p.Nb * 4);
+  w.off_qcnt = o; o = align256(o + size_t(p.BH) * p.Nb * 4);
+  w.total = o;
+  return w;
+}
+cudaError_t launch_attn_bwd(const AttnProblem& p, const void* q, const void* k, const void* v,
+                            const void* o, const float* lse, const void* dout,
+                            const int32_t* kv_idx, const int32_t* kv_cnt, void* dq, void* dk,
+                            void* dv, char* ws, cudaStream_t stream);
+
 // MeanPool_n of K and V, fp32 accumulation, bf16 round-to-nearest.
 cudaError_t launch_gt_pool(const void* k, const void* v, int64_t BH, int N, int d, int window,
                            void* kg, void* vg, cudaStream_t stream);

@@ -1,0 +1,101 @@
+"""Block-sparse attention backward (F3; reading R-23) on the GPU vs
+the fp64 oracle.  The GPU rounds P and dS to bf16 for their MMAs and reads
+the bf16 forward output O for D_r = dO.O; each gradient entry sums up to
+N_kept products whose terms carry ~2^-9 relative rounding, so the test bounds
+the error relative to the gradient's scale: max |err| <= 2e-2 max|ref| and
+mean |err| <= 2e-3 max|ref| for each of dQ, dK, dV (the same 2e-2 / 2e-3
+factors as BASELINE.json's forward O tolerance, applied to the scale of the
+quantity); key rows no query keeps are exactly zero."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import asa_oracle as O
+from paper_2508_10774_b200 import inputs
+
+from . import _parity as PT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A(cuda_dev):
+    from paper_2508_10774_b200 import asa
+    return asa
+
+
+def _lists(BH, Nb, rng, density):
+    kv_idx = np.full((BH, Nb, Nb), -1, np.int32)
+    kv_cnt = np.zeros((BH, Nb), np.int32)
+    for u in range(BH):
+        for i in range(Nb):
+            keep = np.flatnonzero(rng.random(Nb) < density)
+            if keep.size == 0:
+                keep = np.array([rng.integers(Nb)])
+            kv_idx[u, i, :keep.size] = keep
+            kv_cnt[u, i] = keep.size
+    return kv_idx, kv_cnt
+
+
+def _check(got, ref, name):
+    g = got.float().cpu().numpy().astype(np.float64)
+    scale = np.abs(ref).max()
+    err = np.abs(g - ref)
+    assert np.isfinite(g).all(), name
+    assert err.max() <= 2e-2 * scale, (name, err.max(), scale)
+    assert err.mean() <= 2e-3 * scale, (name, err.mean(), scale)
+    return err.max() / scale
+
+
+CASES = [(1, 512, 64, 0.5), (2, 300, 128, 0.6), (1, 70, 64, 1.0), (2, 1000, 128, 0.3),
+         (1, 129, 128, 0.7), (1, 2048, 64, 0.2)]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c)))
+def test_backward_parity_given_mask(A, case):
+    BH, N, d, density = case
+    q, k, v = inputs.iid(1, BH, N, d, seed=N + d)
+    do = inputs.iid(1, BH, N, d, seed=N + d + 1)[0]
+    Nb = O.num_blocks(N, 128)
+    kv_idx, kv_cnt = _lists(BH, Nb, np.random.default_rng(N), density)
+    qd, kd, vd, dod = PT.to_dev(q, k, v, do)
+    ki, kc = PT.lists_to_dev(kv_idx, kv_cnt)
+    o, lse = A.blade_bsa_fwd(qd, kd, vd, ki, kc)
+    dq, dk, dv = A.blade_bsa_bwd(qd, kd, vd, o, lse, dod, ki, kc)
+    torch.cuda.synchronize()
+    rq, rk, rv = O.sparse_attention_backward(q, k, v, do, kv_idx, kv_cnt, 128)
+    for got, ref, nm in ((dq, rq, "dq"), (dk, rk, "dk"), (dv, rv, "dv")):
+        _check(got, ref, nm)
+    # key blocks no query keeps: exactly zero gradient
+    for u in range(BH):
+        kept = set(kv_idx[u][kv_idx[u] >= 0].tolist())
+        for j in range(Nb):
+            if j not in kept:
+                assert dk[u, j * 128:(j + 1) * 128].abs().max().item() == 0.0
+                assert dv[u, j * 128:(j + 1) * 128].abs().max().item() == 0.0
+
+
+def test_backward_on_asa_mask_smooth(A):
+    q, k, v = inputs.smooth(1, 2, 1500, 128, (1, 1, 1500), ell=3.0, beta=9.0, seed=2)
+    do = inputs.iid(1, 2, 1500, 128, seed=7)[0]
+    qd, kd, vd, dod = PT.to_dev(q, k, v, do)
+    o, lse, m = A.asa_forward(qd, kd, vd, tau=0.9)
+    dq, dk, dv = A.blade_bsa_bwd(qd, kd, vd, o, lse, dod, m.kv_idx, m.kv_cnt)
+    torch.cuda.synchronize()
+    rq, rk, rv = O.sparse_attention_backward(q, k, v, do, m.kv_idx.cpu().numpy(),
+                                             m.kv_cnt.cpu().numpy(), 128)
+    for got, ref, nm in ((dq, rq, "dq"), (dk, rk, "dk"), (dv, rv, "dv")):
+        _check(got, ref, nm)
+
+
+def test_backward_deterministic(A):
+    q, k, v = inputs.iid(1, 2, 700, 64, seed=1)
+    do = inputs.iid(1, 2, 700, 64, seed=2)[0]
+    qd, kd, vd, dod = PT.to_dev(q, k, v, do)
+    o, lse, m = A.asa_forward(qd, kd, vd, tau=0.8)
+    g1 = A.blade_bsa_bwd(qd, kd, vd, o, lse, dod, m.kv_idx, m.kv_cnt)
+    g2 = A.blade_bsa_bwd(qd, kd, vd, o, lse, dod, m.kv_idx, m.kv_cnt)
+    torch.cuda.synchronize()
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
