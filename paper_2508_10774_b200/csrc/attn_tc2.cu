@@ -19,7 +19,7 @@
 //   warp  8     tcgen05.mma issuer (one thread) + TMEM allocator
 //   warp  9     TMA producer: Q_A, Q_B, then K tiles in consumption order
 //   warp  10    TMA producer: V tiles in consumption order
-//   warp  11    idle (completes the third warpgroup)
+//   warp  11    idle, or block B's MMA issuer under BLADE_ATTN2_ISSUERS=2
 // TMEM (512 columns): S_A [0,128) S_B [128,256) O_A [256, 256+d) O_B [256+d, 256+2d).
 // P (bf16) overwrites the upper half of its S and is the TMEM A operand of
 // P V; S(n+1) of a block is issued after P V(n) of that block (the tensor
@@ -67,6 +67,9 @@ struct Cfg2 {
 };
 
 constexpr int kThreads2 = 384;
+#ifndef BLADE_ATTN2_ISSUERS
+#define BLADE_ATTN2_ISSUERS 1  // MMA-issuing threads; 2 (one per block) measured 24 % slower (Wan 1.50 vs 1.20 ms)
+#endif
 
 #ifdef BLADE_ATTN2_TRACE  // timing experiment: event timeline of one CTA
 __device__ long long g_tr2[12][40];
@@ -213,20 +216,29 @@ __global__ void __launch_bounds__(kThreads2, 1)
         ++g;
       });
     }
-  } else if (warp == 8) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+  } else if (warp == 8 || warp == 11) {
+    // ===================== MMA issuers =====================
+    // With BLADE_ATTN2_ISSUERS == 2, warp 8 issues block A's MMAs and warp 11
+    // block B's: an issuing thread blocks at the tensor pipe's execution pace,
+    // so a single issuer pushing B's MMAs could not answer A's finished P.
+    // Each thread's commits track only its own block's MMAs; the shared rings
+    // are consumed at fixed positions of the interleaved order.
+    const int mine = BLADE_ATTN2_ISSUERS == 2 ? (warp == 8 ? 0 : 1) : -1;
+    if (lane == 0 && (BLADE_ATTN2_ISSUERS == 2 || warp == 8)) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t qbase = smem_u32(sQ), kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
-      int gk = 0, gv = 0;
+      const int mcommon = cnt0 < cnt1 ? cnt0 : cnt1;
+      // position of block t's item k in the interleaved ring order A0 B0 A1 B1 ...
+      auto pos = [&](int t, int k) { return k < mcommon ? 2 * k + t : mcommon + k; };
       tc::mbar_wait(bar_q, 0);
       tc::fence_after_sync();
-      auto issue_S = [&](int t) {  // S_t = Q_t K^T for the next K tile of the ring
-        const int s = gk % C::kRingK;
-        tc::mbar_wait(bar_kfull + s, (gk / C::kRingK) & 1);
+      auto issue_S = [&](int t, int k) {  // S_t = Q_t K^T of block t's item k
+        const int g = pos(t, k);
+        const int s = g % C::kRingK;
+        tc::mbar_wait(bar_kfull + s, (g / C::kRingK) & 1);
         tc::fence_after_sync();
-        TR2(2 + t, gk / 2);
+        TR2(2 + t, k);
         const uint32_t kb = kbase + s * C::kTile, qb = qbase + t * C::kTile;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -236,11 +248,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         tc::commit(bar_s + t);
         tc::commit(bar_kempty + s);
-        ++gk;
       };
-      auto issue_PV = [&](int t, int k) {  // O_t += P_t V for the next V tile of the ring
-        const int s = gv % C::kRingV;
-        tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
+      auto issue_PV = [&](int t, int k) {  // O_t += P_t V of block t's item k
+        const int g = pos(t, k);
+        const int s = g % C::kRingV;
+        tc::mbar_wait(bar_vfull + s, (g / C::kRingV) & 1);
         TR2(8 + t, k);
         tc::mbar_wait(bar_p + t, k & 1);
         tc::fence_after_sync();
@@ -253,24 +265,33 @@ __global__ void __launch_bounds__(kThreads2, 1)
                      (k > 0 || ks > 0) ? 1 : 0);
         tc::commit(bar_pv + t);
         tc::commit(bar_vempty + s);
-        ++gv;
       };
-      if (cnt0 > 0) issue_S(0);
-      if (cnt1 > 0) issue_S(1);
-      const int m = cnt0 > cnt1 ? cnt0 : cnt1;
-      for (int k = 0; k < m; ++k) {
-        if (k < cnt0) {
-          issue_PV(0, k);
-          if (k + 1 < cnt0) issue_S(0);
+      if (mine >= 0) {
+        const int cnt = mine ? cnt1 : cnt0;
+        if (cnt > 0) issue_S(mine, 0);
+        for (int k = 0; k < cnt; ++k) {
+          issue_PV(mine, k);
+          if (k + 1 < cnt) issue_S(mine, k + 1);
         }
-        if (k < cnt1) {
-          issue_PV(1, k);
-          if (k + 1 < cnt1) issue_S(1);
+        if (cnt > 0) tc::mbar_wait(bar_pv + mine, (cnt - 1) & 1);
+      } else {
+        if (cnt0 > 0) issue_S(0, 0);
+        if (cnt1 > 0) issue_S(1, 0);
+        const int m = cnt0 > cnt1 ? cnt0 : cnt1;
+        for (int k = 0; k < m; ++k) {
+          if (k < cnt0) {
+            issue_PV(0, k);
+            if (k + 1 < cnt0) issue_S(0, k + 1);
+          }
+          if (k < cnt1) {
+            issue_PV(1, k);
+            if (k + 1 < cnt1) issue_S(1, k + 1);
+          }
         }
+        // drain: the last commits must land before the CTA's smem is released
+        if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, (cnt0 - 1) & 1);
+        if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, (cnt1 - 1) & 1);
       }
-      // drain: the last commits must land before the CTA's smem is released
-      if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, (cnt0 - 1) & 1);
-      if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, (cnt1 - 1) & 1);
     }
   }
   } else {
