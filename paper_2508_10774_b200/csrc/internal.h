@@ -68,6 +68,7 @@ struct ProbeSelect {
 };
 
 bool probe_tc_supported(int d, int kk, int Nb);
+bool probe_tc_selects();  // selection fused into the probe epilogue?
 cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
                             const void* qs, const void* ks, float* pimp, const ProbeSelect* sel,
                             cudaStream_t stream);

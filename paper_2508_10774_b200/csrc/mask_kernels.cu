@@ -712,6 +712,10 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     ProbeSelect ps{p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done};
     e = launch_probe_tc(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, &ps, stream);
     if (e != cudaSuccess) return e;
+    if (!probe_tc_selects())  // K-mask.3 as its own launch (warm instruction cache)
+      select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
+          pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
+          done);
   } else {
     if (p.kk > PR_ROWS) {
       e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);

@@ -41,7 +41,13 @@ struct PCfg {
   static constexpr int kSmem = kOffMisc + 16 + 8 * 16 * 4 + 2 * 128 * 4 + 2 * 128 * 8 + 1024;
 };
 
-constexpr int kPThreads = 384;  // warps 0-7 softmax, 8 MMA, 9 TMA, 10-11 idle
+constexpr int kPThreads = 384;
+// Selecting in the probe's epilogue runs select.cuh's large unrolled sort once
+// per warp per CTA from a cold instruction cache, after the CTA's tensor work;
+// the separate select kernel (mask_kernels.cu) keeps it warm across rows.
+#ifndef BLADE_PROBE_FUSED_SELECT
+#define BLADE_PROBE_FUSED_SELECT 0
+#endif  // warps 0-7 softmax, 8 MMA, 9 TMA, 10-11 idle
 
 template <int D, int KK>
 __global__ void __launch_bounds__(kPThreads, 1)
@@ -185,12 +191,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // online row max / sum over this half (l.13-15)
       const float m_new = fmaxf(m_run, tmax);
       if (m_new != -INFINITY) {  // a half tile of padding only leaves (M, l) untouched
+        // packed fp32x2 arithmetic: the same roundings as the scalar
+        // (s - M) * scale and tree sum, half the FMA-pipe issue slots
+        const float2 nm2 = make_float2(-m_new, -m_new), sc2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
-        for (int c = 0; c < 64; ++c) s[c] = ex2((s[c] - m_new) * scale_log2);
+        for (int c = 0; c < 64; c += 2) {
+          const float2 x = mul2(add2(make_float2(s[c], s[c + 1]), nm2), sc2);
+          s[c] = ex2(x.x);
+          s[c + 1] = ex2(x.y);
+        }
 #pragma unroll
-        for (int w = 32; w >= 1; w >>= 1)
+        for (int w = 32; w >= 2; w >>= 1)
 #pragma unroll
-          for (int c = 0; c < w; ++c) s[c] += s[c + w];
+          for (int c = 0; c < w; c += 2) {
+            const float2 y = add2(make_float2(s[c], s[c + 1]), make_float2(s[c + w], s[c + w + 1]));
+            s[c] = y.x;
+            s[c + 1] = y.y;
+          }
+        s[0] += s[1];
         if (m_new != m_run) l_run *= double(ex2((m_run - m_new) * scale_log2));
         l_run += double(s[0]);
         m_run = m_new;
@@ -245,7 +263,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   __syncthreads();
   // K-mask.3 fused: the CTA holds complete P_imp rows of its 128 / KK query
   // blocks; one warp selects each (Alg. 1 l.7-10, select.cuh)
-  {
+  if (BLADE_PROBE_FUSED_SELECT) {
     const int ib = row0 / KK + warp;
     if (warp < 128 / KK && ib < Nb) {
       const int64_t row = u * Nb + ib;
@@ -283,6 +301,8 @@ cudaError_t launch_dk(int64_t BH, int N, int Nb, int b, float scale, const void*
 }
 
 }  // namespace
+
+bool probe_tc_selects() { return BLADE_PROBE_FUSED_SELECT != 0; }
 
 bool probe_tc_supported(int d, int kk, int Nb) {
   return (d == 64 || d == 128) && (kk == 16 || kk == 32) && Nb <= 256;
