@@ -12,10 +12,13 @@
 // it; bsa_bwd_transpose_kernel), dQ walks the forward lists, so every output
 // row is written by exactly one CTA (no atomics, deterministic).
 //
-// First GPU version on the legacy tensor path (mma.sync m16n8k16 bf16, fp32
-// accumulate), FlashAttention-2 structure: CTA = 64 rows (keys for dK/dV,
-// queries for dQ), 4 warps x 16 rows, 64-row tiles of the other operand
-// double-buffered with cp.async; P and dS are rounded to bf16 for their MMAs.
+// The dK/dV and dQ products run in the tcgen05 kernels of attn_bwd_tc.cu;
+// the mma.sync kernels below (FlashAttention-2 structure: CTA = 64 rows, 4
+// warps x 16 rows, 64-row tiles of the other operand double-buffered with
+// cp.async) are the legacy-tensor-path baseline, used when a TMA tensor map
+// cannot be built and selectable with -DBLADE_BWD_{DKDV,DQ}_MMA_SYNC for
+// comparison (12.3 ms vs 3.9 ms on the Wan layer).  P and dS are rounded to
+// bf16 for their MMAs in both.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -61,30 +64,35 @@ __global__ void __launch_bounds__(256) bsa_bwd_dot_kernel(const __nv_bfloat16* _
 }
 
 // ---- transposed lists: q_idx[u, j, :] = query blocks i with j in kv_idx[u, i] -
+// CTA = (unit, 32 key blocks j0..j0+31): scans the unit's lists, sets bit i of
+// j's row in a [32][N_b/32] smem bitmap, then one thread per j emits its
+// query blocks in ascending order.
 __global__ void __launch_bounds__(256) bsa_bwd_transpose_kernel(const int32_t* __restrict__ kv_idx,
                                                                const int32_t* __restrict__ kv_cnt,
                                                                int Nb, int32_t* __restrict__ q_idx,
                                                                int32_t* __restrict__ q_cnt) {
-  __shared__ uint32_t bm[kMaxNbBwd][kMaxNbBwd / 32];  // [key block j][query word]
-  const int64_t u = blockIdx.x;
+  __shared__ uint32_t bm[32][kMaxNbBwd / 32];  // [key block j - j0][query word]
+  const int64_t u = blockIdx.y;
+  const int j0 = blockIdx.x * 32;
   const int nw = (Nb + 31) / 32;
-  for (int e = threadIdx.x; e < Nb * nw; e += blockDim.x) bm[e / nw][e % nw] = 0u;
+  for (int e = threadIdx.x; e < 32 * nw; e += blockDim.x) bm[e / nw][e % nw] = 0u;
   __syncthreads();
   const int32_t* li = kv_idx + u * Nb * Nb;
   const int32_t* lc = kv_cnt + u * Nb;
   for (int e = threadIdx.x; e < Nb * Nb; e += blockDim.x) {
     const int i = e / Nb, k = e % Nb;
-    if (k < lc[i]) {
-      const int j = li[e];
-      atomicOr(&bm[j][i >> 5], 1u << (i & 31));
+    if (k < __ldg(lc + i)) {
+      const int j = __ldg(li + e) - j0;
+      if (j >= 0 && j < 32) atomicOr(&bm[j][i >> 5], 1u << (i & 31));
     }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < Nb; j += blockDim.x) {
+  if (threadIdx.x < 32 && j0 + int(threadIdx.x) < Nb) {
+    const int j = j0 + threadIdx.x;
     int32_t* out = q_idx + (u * Nb + j) * Nb;
     int n = 0;
     for (int w = 0; w < nw; ++w) {
-      uint32_t bits = bm[j][w];
+      uint32_t bits = bm[threadIdx.x][w];
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1;
@@ -373,7 +381,8 @@ cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, con
   const int64_t rows = p.BH * p.N;
   bsa_bwd_dot_kernel<D><<<unsigned((rows * (D / 8) + 255) / 256), 256, 0, stream>>>(
       B(o), B(dout), rows, Dvec);
-  bsa_bwd_transpose_kernel<<<unsigned(p.BH), 256, 0, stream>>>(kv_idx, kv_cnt, p.Nb, q_idx, q_cnt);
+  bsa_bwd_transpose_kernel<<<dim3(unsigned((p.Nb + 31) / 32), unsigned(p.BH)), 256, 0, stream>>>(
+      kv_idx, kv_cnt, p.Nb, q_idx, q_cnt);
   constexpr int TB = BW_TILE * D * 2;
   const int smem_kv = 6 * TB + 4 * BW_TILE * 4;
   const int smem_q = 6 * TB;
@@ -384,9 +393,22 @@ cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, con
                            smem_q);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(2 * p.Nb), unsigned(p.BH));
-  bsa_bwd_dkdv_kernel<D><<<grid, BW_THREADS, smem_kv, stream>>>(
-      B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, q_idx, q_cnt,
-      reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
+  bool dkdv_done = false;
+#ifndef BLADE_BWD_DKDV_MMA_SYNC
+  e = launch_bwd_dkdv_tc(p, q, k, v, lse, dout, Dvec, q_idx, q_cnt, dk, dv, stream);
+  if (e != cudaSuccess && e != cudaErrorNotSupported) return e;
+  dkdv_done = e == cudaSuccess;
+#endif
+  if (!dkdv_done)
+    bsa_bwd_dkdv_kernel<D><<<grid, BW_THREADS, smem_kv, stream>>>(
+        B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, q_idx, q_cnt,
+        reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+#ifndef BLADE_BWD_DQ_MMA_SYNC
+  e = launch_bwd_dq_tc(p, q, k, v, lse, dout, Dvec, kv_idx, kv_cnt, dq, stream);
+  if (e != cudaErrorNotSupported) return e;
+#endif
   bsa_bwd_dq_kernel<D><<<grid, BW_THREADS, smem_q, stream>>>(
       B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, kv_idx, kv_cnt,
       reinterpret_cast<__nv_bfloat16*>(dq));

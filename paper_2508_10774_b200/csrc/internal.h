@@ -120,6 +120,17 @@ cudaError_t launch_attn_bwd(const AttnProblem& p, const void* q, const void* k, 
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* dq, void* dk,
                             void* dv, char* ws, cudaStream_t stream);
 
+// dQ of the backward on tcgen05 (attn_bwd_tc.cu); cudaErrorNotSupported if the
+// tensor maps cannot be built.
+cudaError_t launch_bwd_dkdv_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
+                               const float* lse, const void* dout, const float* Dv,
+                               const int32_t* q_idx, const int32_t* q_cnt, void* dk, void* dv,
+                               cudaStream_t stream);
+cudaError_t launch_bwd_dq_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
+                             const float* lse, const void* dout, const float* Dv,
+                             const int32_t* kv_idx, const int32_t* kv_cnt, void* dq,
+                             cudaStream_t stream);
+
 // MeanPool_n of K and V, fp32 accumulation, bf16 round-to-nearest.
 cudaError_t launch_gt_pool(const void* k, const void* v, int64_t BH, int N, int d, int window,
                            void* kg, void* vg, cudaStream_t stream);

@@ -52,7 +52,7 @@ def main():
     print(json.dumps({"workload": args.workload, "keep": keep, "ms_bwd": ms,
                       "tflops": flop / (ms * 1e-3) / 1e12,
                       "frac_bf16_peak": flop / (ms * 1e-3) / 1e12 / peak,
-                      "kernel": "mma.sync (legacy tensor path) first version"}))
+                      "kernels": "tcgen05: bwd_dkdv_tc_kernel (transposed lists) + bwd_dq_tc_kernel; D_r and list transpose on CUDA cores"}))
 
 
 if __name__ == "__main__":
