@@ -19,7 +19,8 @@
 //   warp  8     tcgen05.mma issuer (one thread) + TMEM allocator
 //   warp  9     TMA producer: Q_A, Q_B, then K tiles in consumption order
 //   warp  10    TMA producer: V tiles in consumption order
-//   warp  11    idle, or block B's MMA issuer under BLADE_ATTN2_ISSUERS=2
+//   warp  11    idle (an issuer per block was measured 24 % slower: an
+//               issuing thread blocks at the tensor pipe's pace either way)
 // TMEM (512 columns): S_A [0,128) S_B [128,256) O_A [256, 256+d) O_B [256+d, 256+2d).
 // P (bf16) overwrites the upper half of its S and is the TMEM A operand of
 // P V; S(n+1) of a block is issued after P V(n) of that block (the tensor
@@ -60,16 +61,22 @@ struct Cfg2 {
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
   static constexpr int kOffBar = kOffRingV + kRingV * kTile;
   // bar_q, kfull/kempty, vfull/vempty, per block: s, p, pv
-  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 3 * 2;
+  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 4 * 2;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
   static constexpr int kSmem = kOffMisc + 16 + 1024;  // + alignment slack
   static constexpr uint32_t kColO = 256;
+  // d = 64 leaves TMEM room for P outside S: P_t at [256 + 2d + 64t, +64), so
+  // S_t(n+1) can be issued as soon as the softmax has read S_t(n).  Parity
+  // green, but measured no faster on the Cog layer (1.05 vs 1.04 ms: the
+  // softmax, not the S round trip, bounds d = 64), so off by default.
+#ifndef BLADE_ATTN2_SEP_P
+#define BLADE_ATTN2_SEP_P 0
+#endif
+  static constexpr bool kSepP = D == 64 && BLADE_ATTN2_SEP_P;
+  static constexpr uint32_t kColP = 256 + 2 * D;
 };
 
 constexpr int kThreads2 = 384;
-#ifndef BLADE_ATTN2_ISSUERS
-#define BLADE_ATTN2_ISSUERS 1  // MMA-issuing threads; 2 (one per block) measured 24 % slower (Wan 1.50 vs 1.20 ms)
-#endif
 
 #ifdef BLADE_ATTN2_TRACE  // timing experiment: event timeline of one CTA
 __device__ long long g_tr2[12][40];
@@ -125,6 +132,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint64_t* bar_s = bar_vempty + C::kRingV;  // [2] S of block t computed
   uint64_t* bar_p = bar_s + 2;               // [2] P of block t written (4 warp arrivals)
   uint64_t* bar_pv = bar_p + 2;              // [2] P V of block t done
+  uint64_t* bar_sf = bar_pv + 2;             // [2] S of block t read out (kSepP, 4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -152,6 +160,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::mbar_init(bar_s + t, 1);
       tc::mbar_init(bar_p + t, 4);
       tc::mbar_init(bar_pv + t, 1);
+      tc::mbar_init(bar_sf + t, 4);
     }
     tc::fence_barrier_init();
   }
@@ -216,27 +225,18 @@ __global__ void __launch_bounds__(kThreads2, 1)
         ++g;
       });
     }
-  } else if (warp == 8 || warp == 11) {
-    // ===================== MMA issuers =====================
-    // With BLADE_ATTN2_ISSUERS == 2, warp 8 issues block A's MMAs and warp 11
-    // block B's: an issuing thread blocks at the tensor pipe's execution pace,
-    // so a single issuer pushing B's MMAs could not answer A's finished P.
-    // Each thread's commits track only its own block's MMAs; the shared rings
-    // are consumed at fixed positions of the interleaved order.
-    const int mine = BLADE_ATTN2_ISSUERS == 2 ? (warp == 8 ? 0 : 1) : -1;
-    if (lane == 0 && (BLADE_ATTN2_ISSUERS == 2 || warp == 8)) {
+  } else if (warp == 8) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t qbase = smem_u32(sQ), kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
-      const int mcommon = cnt0 < cnt1 ? cnt0 : cnt1;
-      // position of block t's item k in the interleaved ring order A0 B0 A1 B1 ...
-      auto pos = [&](int t, int k) { return k < mcommon ? 2 * k + t : mcommon + k; };
+      int gk = 0, gv = 0;  // ring positions (interleaved order A0 B0 A1 B1 ...)
       tc::mbar_wait(bar_q, 0);
       tc::fence_after_sync();
       auto issue_S = [&](int t, int k) {  // S_t = Q_t K^T of block t's item k
-        const int g = pos(t, k);
-        const int s = g % C::kRingK;
-        tc::mbar_wait(bar_kfull + s, (g / C::kRingK) & 1);
+        const int s = gk % C::kRingK;
+        tc::mbar_wait(bar_kfull + s, (gk / C::kRingK) & 1);
         tc::fence_after_sync();
         TR2(2 + t, k);
         const uint32_t kb = kbase + s * C::kTile, qb = qbase + t * C::kTile;
@@ -248,37 +248,42 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         tc::commit(bar_s + t);
         tc::commit(bar_kempty + s);
+        ++gk;
       };
       auto issue_PV = [&](int t, int k) {  // O_t += P_t V of block t's item k
-        const int g = pos(t, k);
-        const int s = g % C::kRingV;
-        tc::mbar_wait(bar_vfull + s, (g / C::kRingV) & 1);
+        const int s = gv % C::kRingV;
+        tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
         TR2(8 + t, k);
         tc::mbar_wait(bar_p + t, k & 1);
         tc::fence_after_sync();
         TR2(4 + t, k);
         const uint32_t vb = vbase + s * C::kTile;
+        const uint32_t pcol = C::kSepP ? C::kColP + t * 64 : t * 128 + 64;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          tc::mma_ts(tmem + C::kColO + t * D, tmem + t * 128 + 64 + ks * 8,
+          tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
                      tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                      (k > 0 || ks > 0) ? 1 : 0);
         tc::commit(bar_pv + t);
         tc::commit(bar_vempty + s);
+        ++gv;
       };
-      if (mine >= 0) {
-        const int cnt = mine ? cnt1 : cnt0;
-        if (cnt > 0) issue_S(mine, 0);
-        for (int k = 0; k < cnt; ++k) {
-          issue_PV(mine, k);
-          if (k + 1 < cnt) issue_S(mine, k + 1);
-        }
-        if (cnt > 0) tc::mbar_wait(bar_pv + mine, (cnt - 1) & 1);
-      } else {
-        if (cnt0 > 0) issue_S(0, 0);
-        if (cnt1 > 0) issue_S(1, 0);
-        const int m = cnt0 > cnt1 ? cnt0 : cnt1;
-        for (int k = 0; k < m; ++k) {
+      if (cnt0 > 0) issue_S(0, 0);
+      if (cnt1 > 0) issue_S(1, 0);
+      const int m = cnt0 > cnt1 ? cnt0 : cnt1;
+      for (int k = 0; k < m; ++k) {
+        if (C::kSepP) {
+          // S(k+1) of both blocks as soon as their S(k) has been read out, then
+          // the P V of item k: the tensor core computes S(k+1) while the
+          // softmax turns S(k) into P(k)
+          for (int t = 0; t < 2; ++t)
+            if (k + 1 < (t ? cnt1 : cnt0)) {
+              tc::mbar_wait(bar_sf + t, k & 1);
+              issue_S(t, k + 1);
+            }
+          if (k < cnt0) issue_PV(0, k);
+          if (k < cnt1) issue_PV(1, k);
+        } else {
           if (k < cnt0) {
             issue_PV(0, k);
             if (k + 1 < cnt0) issue_S(0, k + 1);
@@ -288,10 +293,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
             if (k + 1 < cnt1) issue_S(1, k + 1);
           }
         }
-        // drain: the last commits must land before the CTA's smem is released
-        if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, (cnt0 - 1) & 1);
-        if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, (cnt1 - 1) & 1);
       }
+      // drain: the last commits must land before the CTA's smem is released
+      if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, (cnt0 - 1) & 1);
+      if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, (cnt1 - 1) & 1);
     }
   }
   } else {
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
 #ifdef BLADE_ATTN2_SKIP_SOFTMAX  // timing experiment only: MMA / TMA pipeline alone
       tc::fence_before_sync();
       __syncwarp();
+      if (lane == 0 && C::kSepP) tc::mbar_arrive(bar_sf + t);
       if (lane == 0) tc::mbar_arrive(bar_p + t);
       continue;
 #endif
@@ -328,6 +334,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
       }
       tc::wait_ld();
+      if (C::kSepP) {  // S_t's columns may be overwritten by S_t(n+1) now
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar_sf + t);
+      }
       const bool fine = !kGT || n < cnt_fine;
       const int valid = fine ? N - jb * 128 : gt.Ng - (n - cnt_fine) * 128;
       if (valid < 128) {
@@ -354,8 +365,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
                    fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
       }
       const float mxs = mx * scale_log2;
+      if (C::kSepP && n > 0) {  // P V_t(n-1) done: O_t current and P_t's columns free
+        tc::mbar_wait(bar_pv + t, (n - 1) & 1);
+        tc::fence_after_sync();
+      }
       // warp-uniform (tcgen05.ld/st are .sync.aligned); always true for n = 0.
-      // O_t is current: S_t(n) was issued after P V_t(n-1) and has completed.
+      // O_t is current (kSepP: waited above; else S_t(n) was issued after
+      // P V_t(n-1) and has completed).
       if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
         const float m_new = fmaxf(m_used, mxs);
         if (n > 0) {
@@ -393,7 +409,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
           acc4[e & 3] = add2(acc4[e & 3], pp);
           pk[e] = pack_bf16(pp.x, pp.y);
         }
-        tc::st_32x32b_x16(tS + 64 + c * 16, pk);
+        tc::st_32x32b_x16(C::kSepP ? tmem + lane_base + C::kColP + t * 64 + c * 16
+                                   : tS + 64 + c * 16,
+                          pk);
       }
       const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
       l_sum += acc.x + acc.y;
