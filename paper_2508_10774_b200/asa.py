@@ -193,10 +193,11 @@ def blade_asa_mask(q: torch.Tensor, k: torch.Tensor, *, tau: float = 0.9, keep_m
                         if want_samples else None),
             n_refined=torch.empty(1, dtype=torch.int32, device=dev))
     nbytes = _lib.blade_asa_mask_workspace_size(BH, N, d, ctypes.byref(prm))
-    if nbytes == 0:
-        st = _lib.blade_asa_mask(None, None, BH, N, d, ctypes.byref(prm), None, None, None, None,
-                                 None, None, None, 0, None)
-        raise BladeError(st if st else BLADE_ERR_INVALID_ARG, "blade_asa_mask_workspace_size")
+    if nbytes == 0:  # let the call itself classify the arguments (no work is enqueued)
+        st = _lib.blade_asa_mask(_ptr(q), _ptr(k), BH, N, d, ctypes.byref(prm), None,
+                                 _ptr(out.kv_idx), _ptr(out.kv_cnt), None, None, None, None, 0,
+                                 None)
+        raise BladeError(st if st else BLADE_ERR_INVALID_ARG, "blade_asa_mask")
     ws = _workspace(nbytes, dev, "mask")
     st = _lib.blade_asa_mask(_ptr(q), _ptr(k), BH, N, d, ctypes.byref(prm), _ptr(out.mask),
                              _ptr(out.kv_idx), _ptr(out.kv_cnt), _ptr(out.p_imp),
