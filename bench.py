@@ -298,7 +298,7 @@ def run_stack(args, ws, rank, local, dev):
                        "layer's O to rank 0 inside the step",
                        "l2": "inputs larger than L2, no flush"},
             "ms_per_layer": ms / args.layers, "clocks": clocks,
-            "gpu_launches": 4 * args.layers * args.steps}), flush=True)
+            "gpu_launches": 5 * args.layers * args.steps}), flush=True)
 
 
 def main():
@@ -445,7 +445,7 @@ def main():
         gather = {"bytes_to_rank0": (ws - 1) * o_local.numel() * 2,
                   "seconds_wallclock": time.perf_counter() - g0,
                   "shape": list(o_all.shape) if o_all is not None else None}
-    launches_per_step = 4 + int(gt)  # [gt_pool], sample_gather, probe(+select), refine, attention
+    launches_per_step = 5 + int(gt)  # [gt_pool], sample_gather, probe, select, refine, attention
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws,
