@@ -286,6 +286,7 @@ def run_stack(args, ws, rank, local, dev):
     clocks = clk.stop()
     ms = shard.max_over_ranks([e0.elapsed_time(e1) / args.steps], device=dev)[0]
     flop_all = shard.sum_over_ranks([flop], device=dev)[0]
+    flop_max = shard.max_over_ranks([flop], device=dev)[0]
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": flop_all / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
@@ -298,6 +299,7 @@ def run_stack(args, ws, rank, local, dev):
                        "layer's O to rank 0 inside the step",
                        "l2": "inputs larger than L2, no flush"},
             "ms_per_layer": ms / args.layers, "clocks": clocks,
+            "rank_imbalance_active_flop": flop_max / (flop_all / ws),
             "gpu_launches": 5 * args.layers * args.steps}), flush=True)
 
 
@@ -388,6 +390,7 @@ def main():
     from paper_2508_10774_b200 import shard
     total_ms, attn_ms, mask_ms = shard.max_over_ranks([total_ms, attn_ms, mask_ms], device=dev)
     flop_all = shard.sum_over_ranks([flop], device=dev)[0]
+    flop_max = shard.max_over_ranks([flop], device=dev)[0]
     ms_per_step = total_ms / args.steps
     value = flop_all / (ms_per_step * 1e-3) / 1e12
 
@@ -464,6 +467,7 @@ def main():
             "ms_mask": mask_ms, "ms_attn": attn_ms,
             "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
+            "rank_imbalance_active_flop": flop_max / (flop_all / ws),
             "gather": gather,
         }
         print(json.dumps(line), flush=True)
