@@ -57,7 +57,7 @@ def parse():
                     help="keep-ratio mode: lo = hi = KEEP blocks per row (default 51 wan / 25 cog)")
     ap.add_argument("--tau-mode", action="store_true", help="pure tau mode (lo=ceil(.05 Nb), hi=Nb)")
     ap.add_argument("--tau", type=float, default=0.9)
-    ap.add_argument("--attn", default="auto", choices=["auto", "tcgen05", "mma", "pair"])
+    ap.add_argument("--attn", default="auto", choices=["auto", "tcgen05", "mma", "pair", "triple"])
     ap.add_argument("--variant", default="asa", choices=["asa", "asa_gt"],
                     help="asa_gt: ASA with global tokens (P:135), MeanPool window --window")
     ap.add_argument("--window", type=int, default=128)
@@ -334,7 +334,7 @@ def main():
     Nb = (N + 127) // 128
     mp, mode = mask_params(w, args, Nb)
     impl = {"auto": A.ATTN_AUTO, "tcgen05": A.ATTN_TCGEN05, "mma": A.ATTN_MMA_SYNC,
-            "pair": A.ATTN_TCGEN05_PAIR}[args.attn]
+            "pair": A.ATTN_TCGEN05_PAIR, "triple": A.ATTN_TCGEN05_TRIPLE}[args.attn]
     q, k, v = (t.to(dev) for t in (q_h, k_h, v_h))
     stream = torch.cuda.current_stream()
     unit_offset = rank * w.H

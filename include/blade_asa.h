@@ -108,6 +108,7 @@ size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t bl
 #define BLADE_ATTN_TCGEN05 1   /* sm_100a tcgen05 + TMEM + TMA warp-specialised kernel */
 #define BLADE_ATTN_MMA_SYNC 2  /* legacy mma.sync baseline (kept for comparison)       */
 #define BLADE_ATTN_TCGEN05_PAIR 3 /* tcgen05 kernel with two query blocks per CTA (ping-pong) */
+#define BLADE_ATTN_TCGEN05_TRIPLE 4 /* tcgen05 kernel, one query block, three S buffers  */
 
 /*
  * blade_bsa_fwd — block-sparse attention over kept blocks.

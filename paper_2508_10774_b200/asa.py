@@ -27,7 +27,7 @@ if not os.path.exists(_LIB_PATH):
 _lib = ctypes.CDLL(_LIB_PATH)
 
 BLADE_OK, BLADE_ERR_INVALID_ARG, BLADE_ERR_UNSUPPORTED, BLADE_ERR_WORKSPACE, BLADE_ERR_CUDA = range(5)
-ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC, ATTN_TCGEN05_PAIR = 0, 1, 2, 3
+ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC, ATTN_TCGEN05_PAIR, ATTN_TCGEN05_TRIPLE = 0, 1, 2, 3, 4
 
 ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd_workspace_size",
                "blade_bsa_fwd", "blade_bsa_bwd_workspace_size", "blade_bsa_bwd",

@@ -106,7 +106,7 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   if (!q || !k || !v || !kv_idx || !kv_cnt || !o) return BLADE_ERR_INVALID_ARG;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
   if (BH < 1 || N < 1 || block < 1 || !(scale > 0.f) || !isfinite(scale)) return BLADE_ERR_INVALID_ARG;
-  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_PAIR) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
   if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
@@ -123,6 +123,9 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
     e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
   } else if (pair) {
     e = blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
+    if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
+  } else if (impl == BLADE_ATTN_TCGEN05_TRIPLE) {
+    e = blade::launch_attn_tc3(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
     if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   } else {
     e = blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
@@ -158,7 +161,7 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
     return BLADE_ERR_INVALID_ARG;
   if (BH < 1 || N < 1 || block < 1 || window < 1 || !(scale > 0.f) || !isfinite(scale))
     return BLADE_ERR_INVALID_ARG;
-  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_PAIR) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
   if (block != kGpuBlock || (d != 64 && d != 128) || impl == BLADE_ATTN_MMA_SYNC)
     return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
@@ -169,7 +172,10 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
     return BLADE_ERR_WORKSPACE;
   const blade::GtProblem g{kg, vg, int((int64_t(N) + window - 1) / window), int(window)};
   cudaError_t e =
-      (impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64))
+      impl == BLADE_ATTN_TCGEN05_TRIPLE
+          ? blade::launch_attn_tc3(p, q, k, v, kv_idx, kv_cnt, o, lse,
+                                   static_cast<cudaStream_t>(stream), &g)
+      : (impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64))
           ? blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse,
                                    static_cast<cudaStream_t>(stream), &g)
           : blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,

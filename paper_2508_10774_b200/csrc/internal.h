@@ -131,6 +131,11 @@ cudaError_t launch_bwd_dq_tc(const AttnProblem& p, const void* q, const void* k,
                              const int32_t* kv_idx, const int32_t* kv_cnt, void* dq,
                              cudaStream_t stream);
 
+// One query block per CTA, three S buffers in TMEM (attn_tc3.cu).
+cudaError_t launch_attn_tc3(const AttnProblem& p, const void* q, const void* k, const void* v,
+                            const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
+                            cudaStream_t stream, const GtProblem* gt = nullptr);
+
 // MeanPool_n of K and V, fp32 accumulation, bf16 round-to-nearest.
 cudaError_t launch_gt_pool(const void* k, const void* v, int64_t BH, int N, int d, int window,
                            void* kg, void* vg, cudaStream_t stream);

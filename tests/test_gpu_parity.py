@@ -22,7 +22,8 @@ def A(cuda_dev):
     return asa
 
 
-IMPLS = [pytest.param(2, id="mma_sync"), pytest.param(1, id="tcgen05"), pytest.param(3, id="pair")]
+IMPLS = [pytest.param(2, id="mma_sync"), pytest.param(1, id="tcgen05"), pytest.param(3, id="pair"),
+         pytest.param(4, id="triple")]
 
 
 def _run_mask(A, q, k, p: O.AsaParams, **kw):
