@@ -155,6 +155,30 @@ blade_status_t blade_bsa_bwd(const void* q, const void* k, const void* v, const 
                              const int32_t* kv_cnt, void* dq, void* dk, void* dv,
                              void* workspace, size_t workspace_bytes, void* stream);
 
+/* Bytes of scratch blade_asa_fwd needs (0 on bad args / GPU limits). */
+size_t blade_asa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d,
+                                    const blade_asa_params_t* params);
+
+/*
+ * blade_asa_fwd — the whole ASA forward in one call: blade_asa_mask then
+ * blade_bsa_fwd (P:138-156 then P:133), with the attention launched as a
+ * programmatic dependent of the mask's last kernel (tcgen05 kernels; SURVEY
+ * F4): query blocks whose selection is being recomputed in fp64 wait for it,
+ * every other block starts while it runs.  Results equal the two calls.
+ *   q, k, v     [BH, N, d] bf16 device; params as blade_asa_mask (sample_mode
+ *               0 or 1); impl as blade_bsa_fwd.
+ *   kv_idx, kv_cnt, o, lse   outputs as in the two calls (lse may be NULL);
+ *               kv_cnt is final once the stream has completed.
+ *   workspace   >= blade_asa_fwd_workspace_size().
+ * Errors: as the two calls; UNSUPPORTED after the mask was enqueued leaves
+ * kv_cnt of recomputed rows provisional (negative).
+ */
+blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                             int32_t N, int32_t d, const blade_asa_params_t* params,
+                             int32_t impl, int32_t* kv_idx, int32_t* kv_cnt, void* o,
+                             float* lse, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /*
  * ASA with global tokens, ASA_GT (Step 2.2 (2); readings R-18..R-20):
  * K_aug = Concat(K, MeanPool_n(K)), V_aug likewise.  Window w of the token

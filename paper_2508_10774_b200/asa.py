@@ -30,7 +30,8 @@ BLADE_OK, BLADE_ERR_INVALID_ARG, BLADE_ERR_UNSUPPORTED, BLADE_ERR_WORKSPACE, BLA
 ATTN_AUTO, ATTN_TCGEN05, ATTN_MMA_SYNC, ATTN_TCGEN05_PAIR, ATTN_TCGEN05_TRIPLE = 0, 1, 2, 3, 4
 
 ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd_workspace_size",
-               "blade_bsa_fwd", "blade_bsa_bwd_workspace_size", "blade_bsa_bwd",
+               "blade_bsa_fwd", "blade_asa_fwd_workspace_size", "blade_asa_fwd",
+               "blade_bsa_bwd_workspace_size", "blade_bsa_bwd",
                "blade_gt_pool", "blade_bsa_gt_fwd",
                "blade_gilbert_order", "blade_permute_tokens",
                "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
@@ -59,6 +60,11 @@ _lib.blade_bsa_fwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
 _lib.blade_bsa_fwd.restype = ctypes.c_int
 _lib.blade_bsa_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp, _vp,
                                _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_asa_fwd_workspace_size.restype = _sz
+_lib.blade_asa_fwd_workspace_size.argtypes = [_i64, _i32, _i32, ctypes.POINTER(BladeAsaParams)]
+_lib.blade_asa_fwd.restype = ctypes.c_int
+_lib.blade_asa_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, ctypes.POINTER(BladeAsaParams),
+                               _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.blade_bsa_bwd_workspace_size.restype = _sz
 _lib.blade_bsa_bwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
 _lib.blade_bsa_bwd.restype = ctypes.c_int
@@ -397,6 +403,37 @@ def blade_asa_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, tau
     if st != BLADE_OK:
         raise BladeError(st, "blade_asa_fwd_host")
     return o, lse
+
+
+def blade_asa_fwd(q, k, v, *, tau: float = 0.9, keep_min: int = 1, keep_max: int = 1 << 30,
+                  samples: int = 16, seed: int = 42, unit_offset: int = 0, impl: int = ATTN_AUTO,
+                  want_lse: bool = True, out=None, stream=None, **mask_kw):
+    """The whole forward in one C call (mask, then attention launched as a
+    programmatic dependent of the mask's fp64 refinement).  Returns
+    (O, LSE, kv_idx, kv_cnt); ``out`` = (o, lse, kv_idx, kv_cnt) to reuse."""
+    q = _as_units(q, "q")
+    k = _as_units(k, "k")
+    v = _as_units(v, "v")
+    BH, N, d = q.shape
+    prm = make_params(d=d, tau=tau, keep_min=keep_min, keep_max=keep_max, samples=samples,
+                      seed=seed, unit_offset=unit_offset, **mask_kw)
+    Nb = num_blocks(N)
+    if out is None:
+        out = (torch.empty_like(q),
+               torch.empty((BH, N), dtype=torch.float32, device=q.device) if want_lse else None,
+               torch.empty((BH, Nb, Nb), dtype=torch.int32, device=q.device),
+               torch.empty((BH, Nb), dtype=torch.int32, device=q.device))
+    o, lse, kv_idx, kv_cnt = out
+    nbytes = _lib.blade_asa_fwd_workspace_size(BH, N, d, ctypes.byref(prm))
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_asa_fwd_workspace_size")
+    ws = _workspace(nbytes, q.device, "fwd")
+    st = _lib.blade_asa_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, ctypes.byref(prm), impl,
+                            _ptr(kv_idx), _ptr(kv_cnt), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(),
+                            _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_asa_fwd")
+    return o, lse, kv_idx, kv_cnt
 
 
 def asa_forward(q, k, v, *, tau: float = 0.9, keep_min: int = 1, keep_max: int = 1 << 30,

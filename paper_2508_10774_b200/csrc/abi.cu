@@ -138,6 +138,56 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
 }
 
+size_t blade_asa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d,
+                                    const blade_asa_params_t* params) {
+  const size_t m = blade_asa_mask_workspace_size(BH, N, d, params);
+  const size_t a = params ? blade_bsa_fwd_workspace_size(BH, N, d, params->block) : 0;
+  if (m == 0 || a == 0) return 0;
+  return blade::align256(m) + a;
+}
+
+blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                             int32_t N, int32_t d, const blade_asa_params_t* params,
+                             int32_t impl, int32_t* kv_idx, int32_t* kv_cnt, void* o,
+                             float* lse, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  if (!q || !k || !v || !kv_idx || !kv_cnt || !o) return BLADE_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
+  MaskProblem mp;
+  blade_status_t st = make_mask_problem(BH, N, d, params, &mp);
+  if (st != BLADE_OK) return st;
+  if (mp.mode == 2) return BLADE_ERR_INVALID_ARG;  // supplied samples: use blade_asa_mask
+  const size_t need = blade_asa_fwd_workspace_size(BH, N, d, params);
+  if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return BLADE_ERR_WORKSPACE;
+  const size_t mws = blade::align256(blade::mask_workspace_layout(mp).total);
+  char* ws = static_cast<char*>(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // programmatic dependent launch of the attention behind K-mask.4 (tcgen05
+  // kernels only): rows K-mask.4 recomputes carry a provisional negative
+  // count, and only their CTAs wait for it (SURVEY F4 "fused mask->attention")
+  const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64);
+  const bool pdl = impl == BLADE_ATTN_AUTO || impl == BLADE_ATTN_TCGEN05 || pair;
+  mp.neg_flagged = pdl ? 1 : 0;
+  cudaError_t e = blade::launch_mask(mp, q, k, nullptr, kv_idx, kv_cnt, nullptr, nullptr, nullptr,
+                                     ws, s);
+  if (e != cudaSuccess) return BLADE_ERR_CUDA;
+  AttnProblem ap{BH, N, d, mp.b, mp.Nb, mp.scale};
+  if (impl == BLADE_ATTN_MMA_SYNC) {
+    e = blade::launch_attn_mma(ap, q, k, v, kv_idx, kv_cnt, o, lse, s);
+  } else if (impl == BLADE_ATTN_TCGEN05_TRIPLE) {
+    e = blade::launch_attn_tc3(ap, q, k, v, kv_idx, kv_cnt, o, lse, s);
+  } else if (pair) {
+    e = blade::launch_attn_tc2(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, nullptr, true);
+  } else {
+    e = blade::launch_attn_tc(ap, q, k, v, kv_idx, kv_cnt, o, lse, ws + mws,
+                              workspace_bytes - mws, s, nullptr, true);
+  }
+  if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
+  return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+
 blade_status_t blade_gt_pool(const void* k, const void* v, int64_t BH, int32_t N, int32_t d,
                              int32_t window, void* kg, void* vg, void* stream) {
   if (!k || !v || !kg || !vg) return BLADE_ERR_INVALID_ARG;

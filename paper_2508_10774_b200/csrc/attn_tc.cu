@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmVg, const GtArgs gt, int N, int Nb,
                    float scale_log2_rt, const int32_t* __restrict__ kv_idx,
                    const int32_t* __restrict__ kv_cnt, __nv_bfloat16* __restrict__ O,
-                   float* __restrict__ LSE, volatile int* dbg) {
+                   float* __restrict__ LSE, volatile int* dbg, int pdl) {
   using C = Cfg<D>;
   const float scale_log2 = kDefaultScale ? DefaultScale<D>::kScaleLog2 : scale_log2_rt;
 #ifdef BLADE_TC_DEBUG
@@ -158,7 +158,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int i = blockIdx.x;
   const int64_t u = blockIdx.y;
   const int64_t row_id = u * Nb + i;
-  const int cnt_fine = kv_cnt[row_id];
+  int cnt_fine = kv_cnt[row_id];
+  if (pdl && cnt_fine < 0) {  // refined row (blade_asa_fwd): wait for K-mask.4's final list
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    cnt_fine = __ldcg(kv_cnt + row_id);
+  }
   // items: the kept blocks, then (ASA_GT) the global-token tiles
   const int cnt = cnt_fine + (kGT ? (gt.Ng + 127) / 128 : 0);
   const int32_t* list = kv_idx + row_id * Nb;
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D>
 cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                      const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                     const GtProblem* g, cudaStream_t stream) {
+                     const GtProblem* g, cudaStream_t stream, bool pdl) {
   CUtensorMap mq, mk, mv, mkg, mvg;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mk, k, p.BH, p.N, D) ||
       !make_tile_map(&mv, v, p.BH, p.N, D))
@@ -570,9 +574,26 @@ cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const v
   memset(dbg_host, 0xff, 64 * sizeof(int));
   cudaHostGetDevicePointer(&dbg_dev, dbg_host, 0);
 #endif
-  kern<<<grid, kThreads, smem, stream>>>(
-      mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
-      reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev);
+  if (pdl) {  // programmatic dependent launch behind the refine kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e,
+                           kv_idx, kv_cnt, reinterpret_cast<__nv_bfloat16*>(o), lse,
+                           static_cast<volatile int*>(dbg_dev), 1);
+    if (e != cudaSuccess) return e;
+  } else {
+    kern<<<grid, kThreads, smem, stream>>>(
+        mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
+        reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev, 0);
+  }
   e = cudaGetLastError();
 #ifdef BLADE_ATTN_TRACE
   {
@@ -627,9 +648,9 @@ size_t attn_tc_workspace(const AttnProblem&) { return 256; }
 
 cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                            const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                           char*, size_t, cudaStream_t stream, const GtProblem* gt) {
-  if (p.d == 64) return launch_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
-  if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
+                           char*, size_t, cudaStream_t stream, const GtProblem* gt, bool pdl) {
+  if (p.d == 64) return launch_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
+  if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
   return cudaErrorNotSupported;
 }
 

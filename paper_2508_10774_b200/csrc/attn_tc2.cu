@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     const __grid_constant__ CUtensorMap tmVg, const GtArgs gt, int N, int Nb,
                     float scale_log2_rt, const int32_t* __restrict__ kv_idx,
                     const int32_t* __restrict__ kv_cnt, __nv_bfloat16* __restrict__ O,
-                    float* __restrict__ LSE) {
+                    float* __restrict__ LSE, int pdl) {
   using C = Cfg2<D>;
   const float scale_log2 = kDefaultScale ? DefaultScale<D>::kScaleLog2 : scale_log2_rt;
   extern __shared__ __align__(1024) char smem_raw[];
@@ -140,8 +140,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int i0 = 2 * blockIdx.x;                // block A; block B = i0 + 1 (if < Nb)
   const int nblk = (i0 + 1 < Nb) ? 2 : 1;
   const int ngt = kGT ? (gt.Ng + 127) / 128 : 0;
-  const int cf0 = kv_cnt[u * Nb + i0];
-  const int cf1 = nblk == 2 ? kv_cnt[u * Nb + i0 + 1] : 0;
+  int cf0 = kv_cnt[u * Nb + i0];
+  int cf1 = nblk == 2 ? kv_cnt[u * Nb + i0 + 1] : 0;
+  if (pdl && (cf0 < 0 || cf1 < 0)) {  // a refined row (blade_asa_fwd): wait for K-mask.4
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    cf0 = __ldcg(kv_cnt + u * Nb + i0);
+    cf1 = nblk == 2 ? __ldcg(kv_cnt + u * Nb + i0 + 1) : 0;
+  }
   const int cnt0 = cf0 + ngt, cnt1 = nblk == 2 ? cf1 + ngt : 0;
   const int32_t* list0 = kv_idx + (u * Nb + i0) * Nb;
   const int32_t* list1 = list0 + Nb;
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
 template <int D>
 cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                       const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                      const GtProblem* g, cudaStream_t stream) {
+                      const GtProblem* g, cudaStream_t stream, bool pdl) {
   CUtensorMap mq, mk, mv, mkg, mvg;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mk, k, p.BH, p.N, D) ||
       !make_tile_map(&mv, v, p.BH, p.N, D))
@@ -482,9 +487,25 @@ cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned((p.Nb + 1) / 2), unsigned(p.BH));
-  kern<<<grid, kThreads2, smem, stream>>>(mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e,
-                                          kv_idx, kv_cnt, reinterpret_cast<__nv_bfloat16*>(o),
-                                          lse);
+  if (pdl) {  // programmatic dependent launch behind the refine kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads2);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e,
+                           kv_idx, kv_cnt, reinterpret_cast<__nv_bfloat16*>(o), lse, 1);
+    if (e != cudaSuccess) return e;
+  } else {
+    kern<<<grid, kThreads2, smem, stream>>>(mq, mk, mv, mkg, mvg, ga, p.N, p.Nb,
+                                            p.scale * kLog2e, kv_idx, kv_cnt,
+                                            reinterpret_cast<__nv_bfloat16*>(o), lse, 0);
+  }
   e = cudaGetLastError();
 #ifdef BLADE_ATTN2_TRACE
   {
@@ -509,9 +530,9 @@ cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const 
 
 cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, const void* v,
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                            cudaStream_t stream, const GtProblem* gt) {
-  if (p.d == 64) return launch2_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
-  if (p.d == 128) return launch2_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
+                            cudaStream_t stream, const GtProblem* gt, bool pdl) {
+  if (p.d == 64) return launch2_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
+  if (p.d == 128) return launch2_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
   return cudaErrorNotSupported;
 }
 

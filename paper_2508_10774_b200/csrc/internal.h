@@ -18,6 +18,7 @@ struct MaskProblem {
   int mode, share_qk;
   int64_t unit_offset;
   double guard;
+  int neg_flagged;  // blade_asa_fwd: refined rows' kv_cnt provisional (-1 - m) until K-mask.4
 };
 
 // Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
@@ -65,6 +66,7 @@ struct ProbeSelect {
   int* counters;
   int32_t* flags;
   int* done;
+  int neg_flagged;
 };
 
 bool probe_tc_supported(int d, int kk, int Nb);
@@ -91,15 +93,17 @@ struct GtProblem {
 };
 
 // Returns cudaErrorNotSupported when the tcgen05 path is not available.
+// pdl: launched as a programmatic dependent of the refine kernel (blade_asa_fwd);
+// CTAs whose kv_cnt is negative (provisional) wait for it to complete.
 cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k,
                            const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
                            void* o, float* lse, char* ws, size_t ws_bytes,
-                           cudaStream_t stream, const GtProblem* gt = nullptr);
+                           cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false);
 
 // Two query blocks per CTA (ping-pong softmax warpgroups), attn_tc2.cu.
 cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, const void* v,
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                            cudaStream_t stream, const GtProblem* gt = nullptr);
+                            cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false);
 
 // Block-sparse attention backward (attn_bwd.cu): workspace = D_r (fp32
 // [BH, N]) + transposed lists q_idx [BH, N_b, N_b] + q_cnt [BH, N_b].

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(
     const float* __restrict__ pimp, int64_t rows, int Nb, double tau, int lo, int hi,
     double guard, uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx,
     int32_t* __restrict__ kv_cnt, int* __restrict__ counters, int32_t* __restrict__ flags,
-    int* __restrict__ done) {
+    int* __restrict__ done, int neg_flagged) {
   __shared__ uint32_t keep_bits[SEL_WARPS][16];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * SEL_WARPS + warp;
@@ -332,6 +332,9 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(
     const int slot = atomicAdd(&counters[0], 1);
     flags[slot] = int32_t(row);
     done[slot] = 0;
+    // fused forward (blade_asa_fwd): mark the row's count provisional (-1 - m)
+    // until K-mask.4 writes the final one; attention CTAs of such rows wait
+    if (neg_flagged) kv_cnt[row] = -1 - kv_cnt[row];
   }
 }
 
@@ -484,6 +487,9 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
   __shared__ int last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kt = tid % CK, hr = tid / CK;
+  // a programmatically dependent attention launch (blade_asa_fwd) may start
+  // now: its CTAs of refined rows wait in griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int nflag = counters[0];
   if (blockIdx.x == 0 && tid == 0 && n_refined) *n_refined = nflag;
   const int NK = Nb * kk;
@@ -709,13 +715,14 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   }
   if (probe_tc_supported(D, p.kk, p.Nb)) {
     // K-mask.2 + K-mask.3 fused: tcgen05 probe, selection in its epilogue
-    ProbeSelect ps{p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done};
+    ProbeSelect ps{p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done,
+                   p.neg_flagged};
     e = launch_probe_tc(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, &ps, stream);
     if (e != cudaSuccess) return e;
     if (!probe_tc_selects())  // K-mask.3 as its own launch (warm instruction cache)
       select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
           pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
-          done);
+          done, p.neg_flagged);
   } else {
     if (p.kk > PR_ROWS) {
       e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);
@@ -733,7 +740,7 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     // trust it inside a 2e-5 band
     select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
         pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard > 2e-5 ? p.guard : 2e-5, mask, kv_idx,
-        kv_cnt, counters, flags, done);
+        kv_cnt, counters, flags, done, p.neg_flagged);
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
   if (p.kk <= 64)

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int slot = atomicAdd(&sel.counters[0], 1);
         sel.flags[slot] = int32_t(row);
         sel.done[slot] = 0;
+        if (sel.neg_flagged) sel.kv_cnt[row] = -1 - sel.kv_cnt[row];
       }
     }
   }

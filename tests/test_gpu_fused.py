@@ -1,0 +1,39 @@
+"""blade_asa_fwd (mask + attention in one call, the attention a programmatic
+dependent of the mask's fp64 refinement) equals blade_asa_mask followed by
+blade_bsa_fwd bit for bit, with no row, a few rows and every row refined."""
+
+import pytest
+import torch
+
+from paper_2508_10774_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A(cuda_dev):
+    from paper_2508_10774_b200 import asa
+    return asa
+
+
+@pytest.mark.parametrize("guard", [0.0, 1e-3, 1e30])
+@pytest.mark.parametrize("d,impl", [(128, 0), (64, 0), (128, 1), (64, 3), (128, 2), (128, 4)])
+def test_fused_equals_two_calls(A, d, impl, guard):
+    q, k, v = inputs.smooth(1, 3, 2000, d, (1, 1, 2000), ell=3.0, beta=9.0, seed=d)
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    kw = dict(tau=0.9, keep_min=2, keep_max=12, refine_guard=guard)
+    o1, l1, m = A.asa_forward(qd, kd, vd, impl=impl, **kw)
+    o2, l2, idx, cnt = A.blade_asa_fwd(qd, kd, vd, impl=impl, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(cnt, m.kv_cnt) and (cnt > 0).all()
+    assert torch.equal(idx, m.kv_idx)
+    assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+    assert torch.equal(l1, l2)
+
+
+def test_fused_repeated_calls_are_stable(A):
+    q, k, v = (t.cuda() for t in inputs.make("tiny", "smooth"))
+    outs = [A.blade_asa_fwd(q, k, v, tau=0.9, refine_guard=1e30) for _ in range(5)]
+    torch.cuda.synchronize()
+    for o, lse, idx, cnt in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(cnt, outs[0][3])
