@@ -184,11 +184,12 @@ blade_status_t blade_asa_fwd_host(const void* q_host, const void* k_host, const 
     BLADE_TRY(cudaStreamWaitEvent(s, eng->out[sl], 0));
     blade_asa_params_t pc = *params;
     pc.unit_offset = params->unit_offset + u0;
-    blade_status_t st = blade_asa_mask(dq, dk, cu, N, d, &pc, nullptr, didx, dcnt, nullptr,
-                                       nullptr, nullptr, ws + w.off_mask, w.mask_ws, s);
-    if (st != BLADE_OK) return st;
-    st = blade_bsa_fwd(dq, dk, dv, cu, N, d, params->block, params->scale, didx, dcnt, dO,
-                       lse_host ? dlse : nullptr, impl, ws + w.off_attn, w.attn_ws, s);
+    // mask + attention as one call (the attention a programmatic dependent of
+    // the mask's refinement); its scratch is the contiguous mask + attention
+    // region of the workspace (same layout blade_asa_fwd expects)
+    blade_status_t st = blade_asa_fwd(dq, dk, dv, cu, N, d, &pc, impl, didx, dcnt, dO,
+                                      lse_host ? dlse : nullptr, ws + w.off_mask,
+                                      w.total - w.off_mask, s);
     if (st != BLADE_OK) return st;
     BLADE_TRY(cudaEventRecord(eng->done[sl], s));
 
