@@ -143,7 +143,8 @@ size_t blade_asa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d,
   const size_t m = blade_asa_mask_workspace_size(BH, N, d, params);
   const size_t a = params ? blade_bsa_fwd_workspace_size(BH, N, d, params->block) : 0;
   if (m == 0 || a == 0) return 0;
-  return blade::align256(m) + a;
+  const int64_t Nb = (int64_t(N) + params->block - 1) / params->block;
+  return blade::align256(m) + blade::align256(a) + blade::align256(size_t(BH) * Nb * 4);
 }
 
 blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_t BH,
@@ -170,6 +171,15 @@ blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_
   const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64);
   const bool pdl = impl == BLADE_ATTN_AUTO || impl == BLADE_ATTN_TCGEN05 || pair;
   mp.neg_flagged = pdl ? 1 : 0;
+  // LPT order of the attention CTAs when the counts vary (lo < hi); in
+  // keep-ratio mode every row keeps the same number of blocks
+  const size_t aws = blade::align256(blade_bsa_fwd_workspace_size(BH, N, d, mp.b));
+  int32_t* order = nullptr;
+  if (pdl && mp.lo < mp.hi) {
+    order = reinterpret_cast<int32_t*>(ws + mws + aws);
+    mp.lpt_order = order;
+    mp.lpt_pairs = pair ? 1 : 0;
+  }
   cudaError_t e = blade::launch_mask(mp, q, k, nullptr, kv_idx, kv_cnt, nullptr, nullptr, nullptr,
                                      ws, s);
   if (e != cudaSuccess) return BLADE_ERR_CUDA;
@@ -179,10 +189,10 @@ blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_
   } else if (impl == BLADE_ATTN_TCGEN05_TRIPLE) {
     e = blade::launch_attn_tc3(ap, q, k, v, kv_idx, kv_cnt, o, lse, s);
   } else if (pair) {
-    e = blade::launch_attn_tc2(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, nullptr, true);
+    e = blade::launch_attn_tc2(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, nullptr, true, order);
   } else {
-    e = blade::launch_attn_tc(ap, q, k, v, kv_idx, kv_cnt, o, lse, ws + mws,
-                              workspace_bytes - mws, s, nullptr, true);
+    e = blade::launch_attn_tc(ap, q, k, v, kv_idx, kv_cnt, o, lse, ws + mws, aws, s, nullptr,
+                              true, order);
   }
   if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;

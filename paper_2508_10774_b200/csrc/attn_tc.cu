@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmVg, const GtArgs gt, int N, int Nb,
                    float scale_log2_rt, const int32_t* __restrict__ kv_idx,
                    const int32_t* __restrict__ kv_cnt, __nv_bfloat16* __restrict__ O,
-                   float* __restrict__ LSE, volatile int* dbg, int pdl) {
+                   float* __restrict__ LSE, volatile int* dbg, int pdl,
+                   const int32_t* __restrict__ order) {
   using C = Cfg<D>;
   const float scale_log2 = kDefaultScale ? DefaultScale<D>::kScaleLog2 : scale_log2_rt;
 #ifdef BLADE_TC_DEBUG
@@ -155,9 +156,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef BLADE_ATTN_TIMING
   const long long t_cta0 = clock64();
 #endif
-  const int i = blockIdx.x;
-  const int64_t u = blockIdx.y;
-  const int64_t row_id = u * Nb + i;
+  // LPT order (blade_asa_fwd, tau mode): CTA b takes the b-th longest row
+  const int64_t row_id = order ? int64_t(__ldg(order + blockIdx.y * int64_t(gridDim.x) + blockIdx.x))
+                               : blockIdx.y * int64_t(Nb) + blockIdx.x;
+  const int i = int(row_id % Nb);
+  const int64_t u = row_id / Nb;
   int cnt_fine = kv_cnt[row_id];
   if (pdl && cnt_fine < 0) {  // refined row (blade_asa_fwd): wait for K-mask.4's final list
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -541,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D>
 cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                      const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                     const GtProblem* g, cudaStream_t stream, bool pdl) {
+                     const GtProblem* g, cudaStream_t stream, bool pdl, const int32_t* order) {
   CUtensorMap mq, mk, mv, mkg, mvg;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mk, k, p.BH, p.N, D) ||
       !make_tile_map(&mv, v, p.BH, p.N, D))
@@ -587,12 +590,12 @@ cudaError_t launch_d(const AttnProblem& p, const void* q, const void* k, const v
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e,
                            kv_idx, kv_cnt, reinterpret_cast<__nv_bfloat16*>(o), lse,
-                           static_cast<volatile int*>(dbg_dev), 1);
+                           static_cast<volatile int*>(dbg_dev), 1, order);
     if (e != cudaSuccess) return e;
   } else {
     kern<<<grid, kThreads, smem, stream>>>(
         mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e, kv_idx, kv_cnt,
-        reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev, 0);
+        reinterpret_cast<__nv_bfloat16*>(o), lse, dbg_dev, 0, order);
   }
   e = cudaGetLastError();
 #ifdef BLADE_ATTN_TRACE
@@ -648,9 +651,10 @@ size_t attn_tc_workspace(const AttnProblem&) { return 256; }
 
 cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                            const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                           char*, size_t, cudaStream_t stream, const GtProblem* gt, bool pdl) {
-  if (p.d == 64) return launch_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
-  if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
+                           char*, size_t, cudaStream_t stream, const GtProblem* gt, bool pdl,
+                           const int32_t* order) {
+  if (p.d == 64) return launch_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl, order);
+  if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl, order);
   return cudaErrorNotSupported;
 }
 

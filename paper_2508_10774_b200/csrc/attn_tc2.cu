@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     const __grid_constant__ CUtensorMap tmVg, const GtArgs gt, int N, int Nb,
                     float scale_log2_rt, const int32_t* __restrict__ kv_idx,
                     const int32_t* __restrict__ kv_cnt, __nv_bfloat16* __restrict__ O,
-                    float* __restrict__ LSE, int pdl) {
+                    float* __restrict__ LSE, int pdl, const int32_t* __restrict__ order) {
   using C = Cfg2<D>;
   const float scale_log2 = kDefaultScale ? DefaultScale<D>::kScaleLog2 : scale_log2_rt;
   extern __shared__ __align__(1024) char smem_raw[];
@@ -136,8 +136,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t u = blockIdx.y;
-  const int i0 = 2 * blockIdx.x;                // block A; block B = i0 + 1 (if < Nb)
+  // LPT order (blade_asa_fwd, tau mode): CTA b takes the b-th longest pair
+  const int64_t item = order ? int64_t(__ldg(order + blockIdx.y * int64_t(gridDim.x) + blockIdx.x))
+                             : blockIdx.y * int64_t(gridDim.x) + blockIdx.x;
+  const int64_t u = item / gridDim.x;
+  const int i0 = 2 * int(item % gridDim.x);     // block A; block B = i0 + 1 (if < Nb)
   const int nblk = (i0 + 1 < Nb) ? 2 : 1;
   const int ngt = kGT ? (gt.Ng + 127) / 128 : 0;
   int cf0 = kv_cnt[u * Nb + i0];
@@ -464,7 +467,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
 template <int D>
 cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                       const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                      const GtProblem* g, cudaStream_t stream, bool pdl) {
+                      const GtProblem* g, cudaStream_t stream, bool pdl,
+                      const int32_t* order) {
   CUtensorMap mq, mk, mv, mkg, mvg;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mk, k, p.BH, p.N, D) ||
       !make_tile_map(&mv, v, p.BH, p.N, D))
@@ -499,12 +503,12 @@ cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale * kLog2e,
-                           kv_idx, kv_cnt, reinterpret_cast<__nv_bfloat16*>(o), lse, 1);
+                           kv_idx, kv_cnt, reinterpret_cast<__nv_bfloat16*>(o), lse, 1, order);
     if (e != cudaSuccess) return e;
   } else {
     kern<<<grid, kThreads2, smem, stream>>>(mq, mk, mv, mkg, mvg, ga, p.N, p.Nb,
                                             p.scale * kLog2e, kv_idx, kv_cnt,
-                                            reinterpret_cast<__nv_bfloat16*>(o), lse, 0);
+                                            reinterpret_cast<__nv_bfloat16*>(o), lse, 0, order);
   }
   e = cudaGetLastError();
 #ifdef BLADE_ATTN2_TRACE
@@ -530,9 +534,11 @@ cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const 
 
 cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, const void* v,
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                            cudaStream_t stream, const GtProblem* gt, bool pdl) {
-  if (p.d == 64) return launch2_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
-  if (p.d == 128) return launch2_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl);
+                            cudaStream_t stream, const GtProblem* gt, bool pdl,
+                            const int32_t* order) {
+  if (p.d == 64) return launch2_d<64>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl, order);
+  if (p.d == 128)
+    return launch2_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl, order);
   return cudaErrorNotSupported;
 }
 

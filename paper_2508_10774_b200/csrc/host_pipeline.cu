@@ -59,7 +59,7 @@ DeviceEngines* engines(int dev) {
 }
 
 // Carve-up of the caller's device workspace: two slots of per-chunk tensors,
-// then one mask and one attention scratch (compute is serial on one stream).
+// then one blade_asa_fwd scratch (compute is serial on one stream).
 struct HostWs {
   size_t q, k, v, o, lse, idx, cnt, slot, mask_ws, attn_ws, off_mask, off_attn, total;
 };
@@ -94,11 +94,10 @@ bool sizes(int64_t BH, int32_t N, int32_t d, const blade_asa_params_t* p, int32_
            HostWs* out, int64_t* C_out) {
   if (BH < 1 || N < 1 || !p || chunk_units < 0) return false;
   const int64_t C = auto_chunk(BH, chunk_units);
-  const size_t mws = blade_asa_mask_workspace_size(C, N, d, p);
-  const size_t aws = blade_bsa_fwd_workspace_size(C, N, d, p->block);
-  if (mws == 0 || aws == 0) return false;
+  const size_t fws = blade_asa_fwd_workspace_size(C, N, d, p);  // mask + attention scratch
+  if (fws == 0) return false;
   const int Nb = int((int64_t(N) + p->block - 1) / p->block);
-  *out = host_ws_layout(C, N, d, Nb, mws, aws);
+  *out = host_ws_layout(C, N, d, Nb, fws, 0);
   *C_out = C;
   return true;
 }

@@ -19,6 +19,8 @@ struct MaskProblem {
   int64_t unit_offset;
   double guard;
   int neg_flagged;  // blade_asa_fwd: refined rows' kv_cnt provisional (-1 - m) until K-mask.4
+  int32_t* lpt_order;  // blade_asa_fwd: LPT order of the attention CTAs, written before K-mask.4
+  int lpt_pairs;       // order over pairs of query blocks (two-block kernel)
 };
 
 // Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
@@ -98,12 +100,20 @@ struct GtProblem {
 cudaError_t launch_attn_tc(const AttnProblem& p, const void* q, const void* k,
                            const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
                            void* o, float* lse, char* ws, size_t ws_bytes,
-                           cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false);
+                           cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
+                           const int32_t* order = nullptr);
 
 // Two query blocks per CTA (ping-pong softmax warpgroups), attn_tc2.cu.
 cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, const void* v,
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                            cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false);
+                            cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
+                            const int32_t* order = nullptr);
+
+// Longest-processing-time order of the attention CTAs (one query block, or a
+// pair of blocks when pairs != 0) by kept-block count, descending; counts may
+// be provisional (negative: -1 - m).  order: [BH * ceil(Nb / (pairs ? 2 : 1))].
+cudaError_t launch_lpt_order(const int32_t* kv_cnt, int64_t BH, int Nb, int d, int pairs,
+                             int32_t* order, cudaStream_t stream);
 
 // Block-sparse attention backward (attn_bwd.cu): workspace = D_r (fp32
 // [BH, N]) + transposed lists q_idx [BH, N_b, N_b] + q_cnt [BH, N_b].

@@ -742,6 +742,10 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard > 2e-5 ? p.guard : 2e-5, mask, kv_idx,
         kv_cnt, counters, flags, done, p.neg_flagged);
   }
+  if (p.lpt_order) {  // before K-mask.4, so the attention stays its programmatic dependent
+    e = launch_lpt_order(kv_cnt, p.BH, p.Nb, D, p.lpt_pairs, p.lpt_order, stream);
+    if (e != cudaSuccess) return e;
+  }
   // K-mask.4 (persistent grid; the queue length is read on the device)
   if (p.kk <= 64)
     refine_kernel<D, 64><<<148 * 3, RF_THREADS, 0, stream>>>(
@@ -780,6 +784,73 @@ cudaError_t launch_mask(const MaskProblem& p, const void* q, const void* k, uint
     return launch_mask_d<128>(p, q, k, mask, kv_idx, kv_cnt, p_imp_out, sample_idx, n_refined,
                               ws, stream);
   return cudaErrorInvalidValue;
+}
+
+}  // namespace blade
+
+// ---------------------------------------------------------------------------
+// LPT order of the attention CTAs: with content-adaptive lists the
+// CTAs of a tau-mode call differ in work by up to N_b / lo; launching the
+// longest first keeps the last wave short.  Items (a query block, or a pair
+// of blocks for the two-block kernel) are sorted by kept-block count,
+// descending, WITHIN each unit (one CTA per unit, counting sort): units stay
+// in launch order, so the CTAs in flight keep sharing one unit's K and V in
+// L2 (a global sort mixes every unit's K/V and measured slower on Wan).  The
+// order of equal counts is arbitrary (atomics); it cannot change any result,
+// every CTA writes its own rows.
+// ---------------------------------------------------------------------------
+namespace blade {
+namespace {
+
+constexpr int kLptBins = 2 * kMaxNb + 1;
+
+__global__ void __launch_bounds__(256) lpt_order_kernel(const int32_t* __restrict__ kv_cnt,
+                                                        int64_t BH, int Nb, int pairs,
+                                                        int per_unit, int group,
+                                                        int32_t* __restrict__ order) {
+  __shared__ int hist[kLptBins];
+  const int64_t u0 = int64_t(blockIdx.x) * group;
+  const int64_t u1 = u0 + group < BH ? u0 + group : BH;
+  const int items = int((u1 - u0) * per_unit);
+  for (int b = threadIdx.x; b < kLptBins; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  auto key = [&](int it) {
+    const int64_t u = u0 + it / per_unit;
+    const int x = it % per_unit;
+    auto c = [&](int i) {
+      const int v = kv_cnt[u * Nb + i];
+      return v < 0 ? -1 - v : v;  // provisional count of a row K-mask.4 recomputes
+    };
+    return pairs ? c(2 * x) + (2 * x + 1 < Nb ? c(2 * x + 1) : 0) : c(x);
+  };
+  for (int it = threadIdx.x; it < items; it += blockDim.x) atomicAdd(&hist[key(it)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // descending exclusive scan: start of each count's range
+    int run = 0;
+    for (int b = kLptBins - 1; b >= 0; --b) {
+      const int h = hist[b];
+      hist[b] = run;
+      run += h;
+    }
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < items; it += blockDim.x)
+    order[u0 * per_unit + atomicAdd(&hist[key(it)], 1)] = int32_t(u0 * per_unit + it);
+}
+
+}  // namespace
+
+cudaError_t launch_lpt_order(const int32_t* kv_cnt, int64_t BH, int Nb, int d, int pairs,
+                             int32_t* order, cudaStream_t stream) {
+  const int per_unit = pairs ? (Nb + 1) / 2 : Nb;
+  // sort within groups of units whose K and V fit in about 48 MB of L2
+  const double unit_kv = 2.0 * Nb * 128.0 * d * 2.0;
+  int group = int(48e6 / unit_kv);
+  group = group < 1 ? 1 : group;
+  const int64_t ngroups = (BH + group - 1) / group;
+  lpt_order_kernel<<<unsigned(ngroups), 256, 0, stream>>>(kv_cnt, BH, Nb, pairs, per_unit, group,
+                                                          order);
+  return cudaGetLastError();
 }
 
 }  // namespace blade
