@@ -77,13 +77,27 @@ __global__ void __launch_bounds__(256) bsa_bwd_transpose_kernel(const int32_t* _
   const int nw = (Nb + 31) / 32;
   for (int e = threadIdx.x; e < 32 * nw; e += blockDim.x) bm[e / nw][e % nw] = 0u;
   __syncthreads();
+  __shared__ int scnt[kMaxNbBwd];
   const int32_t* li = kv_idx + u * Nb * Nb;
-  const int32_t* lc = kv_cnt + u * Nb;
-  for (int e = threadIdx.x; e < Nb * Nb; e += blockDim.x) {
-    const int i = e / Nb, k = e % Nb;
-    if (k < __ldg(lc + i)) {
-      const int j = __ldg(li + e) - j0;
-      if (j >= 0 && j < 32) atomicOr(&bm[j][i >> 5], 1u << (i & 31));
+  for (int i = threadIdx.x; i < Nb; i += blockDim.x) scnt[i] = __ldg(kv_cnt + u * Nb + i);
+  __syncthreads();
+  // 8 independent loads in flight per thread (the scan is latency-bound)
+  const int total = Nb * Nb;
+  for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
+    int val[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = base + q * blockDim.x;
+      val[q] = e < total ? __ldg(li + e) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = base + q * blockDim.x;
+      if (e < total) {
+        const int i = e / Nb, k = e % Nb;
+        const int j = val[q] - j0;
+        if (k < scnt[i] && j >= 0 && j < 32) atomicOr(&bm[j][i >> 5], 1u << (i & 31));
+      }
     }
   }
   __syncthreads();
