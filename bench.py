@@ -239,6 +239,26 @@ def run_reference(args, ws, rank):
 # ---------------------------------------------------------------------------
 
 
+# BLADE_BENCH_SHARE_GPU=1 (testing only): every rank uses cuda:0 and gloo, so
+# the multi-rank code path (sharding, max-over-ranks timing, gather) can be
+# exercised on a single-GPU box; numbers measured that way are not bench values.
+_SHARE_GPU = os.environ.get("BLADE_BENCH_SHARE_GPU") == "1"
+
+
+def bind_device(local: int) -> torch.device:
+    idx = 0 if _SHARE_GPU else local
+    torch.cuda.set_device(idx)
+    return torch.device("cuda", idx)
+
+
+def init_dist(dev: torch.device) -> None:
+    import torch.distributed as dist
+    if _SHARE_GPU:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+
+
 def run_stack(args, ws, rank, local, dev):
     """BASELINE.json configs[4]: the Wan2.1-1.3B attention stack, batch 8 x
     30 layers, (batch, head) units sharded over the ranks (strong scaling:
@@ -313,20 +333,16 @@ def main():
         run_reference(args, ws, rank)
         return
     if args.workload == "wan_stack":
-        torch.cuda.set_device(local)
-        dev = torch.device("cuda", local)
+        dev = bind_device(local)
         if ws > 1:
-            import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=dev)
+            init_dist(dev)
         run_stack(args, ws, rank, local, dev)
         if ws > 1:
             torch.distributed.destroy_process_group()
         return
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = bind_device(local)
     if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     from paper_2508_10774_b200 import asa as A
 
     w = inputs.WORKLOADS[args.workload]
