@@ -214,10 +214,17 @@ def run_reference(args, ws, rank):
     mp, mode = mask_params(w, args, Nb)
     vals, secs = [], []
     desc = ""
+    # each step is one bounded sample (~3 s on the Wan layer); the run stops
+    # early once the next step would exceed the time budget, so the arm ends
+    # within a few minutes whatever --steps is (steps_run says how many ran)
+    budget = float(os.environ.get("BLADE_REF_BUDGET_S", "150"))
+    t_start = time.perf_counter()
     for _ in range(args.steps):
         flop, sec, desc = oracle_sample(q, k, v, w, mp, 1, 8 if args.workload != "tiny" else None)
         vals.append(flop / sec / 1e12)
         secs.append(sec)
+        if time.perf_counter() - t_start + sec > budget:
+            break
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
@@ -225,7 +232,8 @@ def run_reference(args, ws, rank):
         "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d, "mask": mode,
-                   "tau": mp["tau"], "sample_per_step": desc},
+                   "tau": mp["tau"], "sample_per_step": desc, "steps_run": len(vals),
+                   "time_budget_s": budget},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores_used(),
                          "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
