@@ -1,6 +1,6 @@
 """Run one small tcgen05 attention call with a host-side watchdog (debug aid)."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_2508_10774_b200 import asa as A, inputs
 from oracle import asa_oracle as O

@@ -1,7 +1,7 @@
 """Measure the fp32 probe error vs the fp64 oracle and the refine-queue size
 per guard value (sets the default refine_guard; R-14)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_2508_10774_b200 import asa as A, inputs
 from oracle import asa_oracle as O
