@@ -483,6 +483,22 @@ def main():
             "traffic": traffic_for(args.workload, "attn"),
             "attn_ms": attn_ms, "mask_ms": mask_ms,
             "attn_share": attn_ms / (attn_ms + mask_ms)}
+    # the mask side: the sampled probe is exponential- (MUFU-)
+    # and tensor-bound, the gather / list writes HBM-bound; all three rates
+    # over the whole blade_asa_mask time (sample, probe, select, refine)
+    nk = sum(min(16, min(128, N - i * 128)) for i in range(Nb))
+    sm_clk = (clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)) * 1e6
+    mufu_peak = 16.0 * 148 * sm_clk  # ex2 per second (16 per clock per SM)
+    exps = BH * nk * nk / (mask_ms * 1e-3)
+    mask_bytes = BH * (2 * nk * d * 2 + Nb * Nb * 4 + Nb * 4)
+    mask_roof = {"bound": "mufu", "basis": "whole blade_asa_mask time",
+                 "exps_per_s": exps, "mufu_peak_exps_per_s": mufu_peak,
+                 "mufu_frac": exps / mufu_peak,
+                 "probe_tflops": probe_flop(BH, N, d) / (mask_ms * 1e-3) / 1e12,
+                 "probe_tensor_frac": probe_flop(BH, N, d) / (mask_ms * 1e-3) / 1e12
+                 / pk["bf16_tflops"],
+                 "hbm_gbs_algorithmic": mask_bytes / (mask_ms * 1e-3) / 1e9,
+                 "hbm_frac": mask_bytes / (mask_ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -520,7 +536,8 @@ def main():
             "step_api": ("blade_asa_fwd (one call; attention a programmatic dependent of the "
                          "mask's last kernel)" if fused_ms is not None else
                          "blade_asa_mask + blade_bsa_fwd"),
-            "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clocks, "e2e": e2e, "roofline": roof, "mask_roofline": mask_roof,
+            "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
             "rank_imbalance_active_flop": flop_max / (flop_all / ws),
             "gather": gather,
