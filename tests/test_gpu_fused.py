@@ -37,3 +37,20 @@ def test_fused_repeated_calls_are_stable(A):
     torch.cuda.synchronize()
     for o, lse, idx, cnt in outs[1:]:
         assert torch.equal(o, outs[0][0]) and torch.equal(cnt, outs[0][3])
+
+
+@pytest.mark.parametrize("N", [1, 129, 300, 1407])
+@pytest.mark.parametrize("d", [64, 128])
+def test_fused_edges_lpt(A, N, d):
+    """Odd block counts (the two-block kernel's lone last block), a single
+    token, tau mode so the LPT order is active, every row refined."""
+    q, k, v = inputs.iid(1, 2, N, d, seed=N + d)
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    for guard in (0.0, 1e30):
+        kw = dict(tau=0.8, keep_min=1, refine_guard=guard)
+        o1, l1, m = A.asa_forward(qd, kd, vd, **kw)
+        o2, l2, idx, cnt = A.blade_asa_fwd(qd, kd, vd, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(cnt, m.kv_cnt) and torch.equal(idx, m.kv_idx)
+        assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+        assert torch.equal(l1, l2)
