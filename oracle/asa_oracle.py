@@ -708,3 +708,51 @@ def sparse_attention_backward(q, k, v, do, kv_idx, kv_cnt, b: int, scale: float 
         dq[u], dk[u], dv[u] = sparse_attention_backward_unit(q[u], k[u], v[u], do[u], kv_idx[u],
                                                              kv_cnt[u], b, scale)
     return dq, dk, dv
+
+
+def sparse_attention_gt_backward_unit(q_u, k_u, v_u, do_u, kv_idx_u, kv_cnt_u, b: int,
+                                      scale: float, n: int):
+    """fp64 (dQ, dK, dV) of ASA_GT attention (F1 + F3).
+    The global tokens are K_g = round_bf16(MeanPool_n(K)) (R-19); the
+    gradient passes through the mean (each token of window w receives 1/n_w
+    of the pooled token's gradient) and through the bf16 rounding as the
+    identity (straight-through: rounding has zero derivative almost
+    everywhere, the training recipe treats K_aug as a function of K).  The
+    mask is a constant (R-23).  Per query block i, with T = kept keys:
+      A = [scale q K_T^T, scale q K_g^T + ln n_w],  P = softmax(A)
+      dV_T += P_T^T dO,   dV_g = P_g^T dO
+      dP = dO [V_T; V_g]^T,  dS = P (dP - rowsum(P dP))
+      dQ += scale dS [K_T; K_g],  dK_T += scale dS_T^T q,  dK_g = scale dS_g^T q
+    then dK[t] += dK_g[w(t)] / n_w, dV[t] += dV_g[w(t)] / n_w."""
+    q_u, k_u, v_u, do_u = to_f64(q_u), to_f64(k_u), to_f64(v_u), to_f64(do_u)
+    N, d = q_u.shape
+    Nb = num_blocks(N, b)
+    kg, vg, bias = global_tokens(k_u, v_u, n)
+    Ng = kg.shape[0]
+    dq, dk, dv = np.zeros_like(q_u), np.zeros_like(k_u), np.zeros_like(v_u)
+    dkg, dvg = np.zeros((Ng, d)), np.zeros((Ng, d))
+    for i in range(Nb):
+        r0, r1 = i * b, min((i + 1) * b, N)
+        cols = np.concatenate([np.arange(j * b, min((j + 1) * b, N))
+                               for j in kv_idx_u[i, :kv_cnt_u[i]]])
+        Kaug = np.concatenate([k_u[cols], kg], axis=0)
+        Vaug = np.concatenate([v_u[cols], vg], axis=0)
+        A = (q_u[r0:r1] @ Kaug.T) * scale
+        A[:, len(cols):] += bias[None, :]
+        P = np.exp(A - A.max(axis=1, keepdims=True))
+        P /= P.sum(axis=1, keepdims=True)
+        dO = do_u[r0:r1]
+        dVaug = P.T @ dO
+        dP = dO @ Vaug.T
+        dS = P * (dP - (P * dP).sum(axis=1, keepdims=True))
+        dq[r0:r1] += scale * (dS @ Kaug)
+        dKaug = scale * (dS.T @ q_u[r0:r1])
+        dk[cols] += dKaug[:len(cols)]
+        dv[cols] += dVaug[:len(cols)]
+        dkg += dKaug[len(cols):]
+        dvg += dVaug[len(cols):]
+    w_of = np.arange(N) // n
+    counts = np.bincount(w_of, minlength=Ng).astype(np.float64)
+    dk += dkg[w_of] / counts[w_of, None]
+    dv += dvg[w_of] / counts[w_of, None]
+    return dq, dk, dv

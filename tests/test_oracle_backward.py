@@ -101,3 +101,39 @@ def test_all_ones_mask_is_dense_backward():
     np.testing.assert_allclose(dq, qt.grad.numpy(), atol=1e-11, rtol=0)
     np.testing.assert_allclose(dk, kt.grad.numpy(), atol=1e-11, rtol=0)
     np.testing.assert_allclose(dv, vt.grad.numpy(), atol=1e-11, rtol=0)
+
+
+@pytest.mark.parametrize("N,d,b,n,seed", [(384, 16, 128, 128, 0), (300, 16, 128, 100, 1),
+                                          (200, 8, 64, 7, 2)])
+def test_gt_backward_equals_autograd(N, d, b, n, seed):
+    """ASA_GT gradients vs torch autograd (fp64) through avg_pool1d (ceil
+    mode) and SDPA over [K; MeanPool_n(K)] with the ln(n_w) additive mask; the
+    oracle's bf16 rounding of the pooled rows is matched by feeding autograd
+    the same rounded values with a straight-through estimator."""
+    q, k, v = (inputs.iid(1, 1, N, d, seed)[i][0].double() for i in range(3))
+    g = torch.from_numpy(np.random.default_rng(seed + 5).standard_normal((N, d)))
+    Nb = O.num_blocks(N, b)
+    kv_idx, kv_cnt = _lists(Nb, np.random.default_rng(seed), 0.5)
+    scale = O.default_scale(d)
+    dq, dk, dv = O.sparse_attention_gt_backward_unit(q.numpy(), k.numpy(), v.numpy(), g.numpy(),
+                                                     kv_idx, kv_cnt, b, scale, n)
+    qt, kt, vt = (x.clone().requires_grad_(True) for x in (q, k, v))
+
+    def pool_ste(x):  # mean over windows, rounded to bf16 in the forward only
+        m = F.avg_pool1d(x.T[None], n, n, ceil_mode=True)[0].T
+        r = m.float().to(torch.bfloat16).double()
+        return m + (r - m).detach()
+
+    kg, vg = pool_ste(kt), pool_ste(vt)
+    Ng = kg.shape[0]
+    nw = torch.tensor([min(n, N - w * n) for w in range(Ng)], dtype=torch.float64)
+    M = _token_mask(kv_idx, kv_cnt, N, b)
+    bias = torch.full((N, N + Ng), float("-inf"), dtype=torch.float64)
+    bias[:, :N][M] = 0.0
+    bias[:, N:] = torch.log(nw)[None, :]
+    out = F.scaled_dot_product_attention(qt[None], torch.cat([kt, kg])[None],
+                                         torch.cat([vt, vg])[None], attn_mask=bias[None],
+                                         scale=scale)[0]
+    out.backward(g)
+    for mine, ref in ((dq, qt.grad), (dk, kt.grad), (dv, vt.grad)):
+        np.testing.assert_allclose(mine, ref.numpy(), rtol=0, atol=1e-10)
