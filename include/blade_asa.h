@@ -212,6 +212,33 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
                                 int32_t impl, void* workspace, size_t workspace_bytes,
                                 void* stream);
 
+/* Bytes of scratch blade_bsa_gt_bwd needs (0 on bad args / GPU limits). */
+size_t blade_bsa_gt_bwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block,
+                                       int32_t window);
+
+/*
+ * blade_bsa_gt_bwd — gradients of blade_bsa_gt_fwd with respect to q, k, v,
+ * the global tokens kg = MeanPool_n(k), vg = MeanPool_n(v) included
+ * (P:135 trained through P:158-161; readings R-23, R-24).  P_rt as in
+ * blade_bsa_bwd with the forward's LSE (which covers the global tokens),
+ * P_rw = exp(scale q_r.kg_w + ln n_w - LSE_r), dS = P (dO.v - D_r):
+ *   dQ_r  = scale (sum_t dS_rt k_t + sum_w dS_rw kg_w),
+ *   dK_t  = scale sum_r dS_rt q_r + dKg_{w(t)} / n_{w(t)},
+ *   dV_t  = sum_r P_rt dO_r       + dVg_{w(t)} / n_{w(t)},
+ *   dKg_w = scale sum_r dS_rw q_r,  dVg_w = sum_r P_rw dO_r over ALL rows r;
+ * the bf16 rounding of kg, vg is passed through as the identity.
+ *   kg, vg      the forward's global tokens [BH, N_g, d] bf16, N_g = ceil(N/window).
+ *   o, lse      blade_bsa_gt_fwd's outputs.  Other arguments as blade_bsa_bwd.
+ *   workspace   >= blade_bsa_gt_bwd_workspace_size().
+ * Deterministic (no atomics).  Errors: INVALID_ARG, UNSUPPORTED, WORKSPACE, CUDA.
+ */
+blade_status_t blade_bsa_gt_bwd(const void* q, const void* k, const void* v, const void* kg,
+                                const void* vg, int32_t window, const void* o, const float* lse,
+                                const void* dout, int64_t BH, int32_t N, int32_t d,
+                                int32_t block, float scale, const int32_t* kv_idx,
+                                const int32_t* kv_cnt, void* dq, void* dk, void* dv,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 /*
  * Locality-preserving token rearrangement ("Gilbert space-filling
  * curve to reorder the tokens before blocking"; Alg. 1 l.1; readings

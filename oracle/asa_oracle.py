@@ -756,3 +756,15 @@ def sparse_attention_gt_backward_unit(q_u, k_u, v_u, do_u, kv_idx_u, kv_cnt_u, b
     dk += dkg[w_of] / counts[w_of, None]
     dv += dvg[w_of] / counts[w_of, None]
     return dq, dk, dv
+
+
+def sparse_attention_gt_backward(q, k, v, do, kv_idx, kv_cnt, b: int, n: int,
+                                 scale: float | None = None, units=None):
+    """F1 + F3 for [BH, N, d]: fp64 dQ, dK, dV of ASA_GT (units not listed are NaN)."""
+    q, k, v, do = to_f64(q), to_f64(k), to_f64(v), to_f64(do)
+    scale = default_scale(q.shape[2]) if scale is None else float(scale)
+    dq, dk, dv = (np.full(q.shape, np.nan) for _ in range(3))
+    for u in (range(q.shape[0]) if units is None else units):
+        dq[u], dk[u], dv[u] = sparse_attention_gt_backward_unit(
+            q[u], k[u], v[u], do[u], kv_idx[u], kv_cnt[u], b, scale, n)
+    return dq, dk, dv

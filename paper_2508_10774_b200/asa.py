@@ -33,6 +33,7 @@ ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd
                "blade_bsa_fwd", "blade_asa_fwd_workspace_size", "blade_asa_fwd",
                "blade_bsa_bwd_workspace_size", "blade_bsa_bwd",
                "blade_gt_pool", "blade_bsa_gt_fwd",
+               "blade_bsa_gt_bwd_workspace_size", "blade_bsa_gt_bwd",
                "blade_gilbert_order", "blade_permute_tokens",
                "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
                "blade_status_string", "blade_version")
@@ -75,6 +76,11 @@ _lib.blade_gt_pool.argtypes = [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]
 _lib.blade_bsa_gt_fwd.restype = ctypes.c_int
 _lib.blade_bsa_gt_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, ctypes.c_float, _vp,
                                   _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _sz, _vp]
+_lib.blade_bsa_gt_bwd_workspace_size.restype = _sz
+_lib.blade_bsa_gt_bwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32, _i32]
+_lib.blade_bsa_gt_bwd.restype = ctypes.c_int
+_lib.blade_bsa_gt_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i32, _i32,
+                                  _i32, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.blade_gilbert_order.restype = ctypes.c_int
 _lib.blade_gilbert_order.argtypes = [_i32, _i32, _i32, _i32, _vp, _i64]
 _lib.blade_permute_tokens.restype = ctypes.c_int
@@ -320,6 +326,36 @@ def blade_bsa_gt_fwd(q, k, v, kv_idx, kv_cnt, kg, vg, *, window: int = 128,
     if st != BLADE_OK:
         raise BladeError(st, "blade_bsa_gt_fwd")
     return o, lse
+
+
+def blade_bsa_gt_bwd(q, k, v, kg, vg, o, lse, do, kv_idx, kv_cnt, *, window: int = 128,
+                     scale: float | None = None, block: int = 128, dq=None, dk=None, dv=None,
+                     stream=None):
+    """Gradients of ASA_GT attention (P:135 trained per P:158-161), through
+    MeanPool_n to K and V -> (dQ, dK, dV) bf16."""
+    q, k, v, o, do = (_as_units(x, n) for x, n in ((q, "q"), (k, "k"), (v, "v"), (o, "o"),
+                                                    (do, "do")))
+    kg, vg = _as_units(kg, "kg"), _as_units(vg, "vg")
+    BH, N, d = q.shape
+    if tuple(kg.shape) != (BH, num_global_tokens(N, window), d) or kg.shape != vg.shape:
+        raise ValueError("kg, vg must be [BH, ceil(N/window), d]")
+    if lse.dtype != torch.float32 or not lse.is_cuda or tuple(lse.shape) != (BH, N):
+        raise ValueError("lse must be CUDA fp32 [BH, N]")
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    nbytes = _lib.blade_bsa_gt_bwd_workspace_size(BH, N, d, block, window)
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_gt_bwd_workspace_size")
+    ws = _workspace(nbytes, q.device, "gt_bwd")
+    st = _lib.blade_bsa_gt_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(kg), _ptr(vg), window, _ptr(o),
+                               _ptr(lse.contiguous()), _ptr(do), BH, N, d, block,
+                               default_scale(d) if scale is None else scale, _ptr(kv_idx),
+                               _ptr(kv_cnt), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(),
+                               _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_bsa_gt_bwd")
+    return dq, dk, dv
 
 
 def asa_gt_forward(q, k, v, *, window: int = 128, tau: float = 0.9, keep_min: int = 1,

@@ -278,6 +278,44 @@ blade_status_t blade_bsa_bwd(const void* q, const void* k, const void* v, const 
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
 }
 
+size_t blade_bsa_gt_bwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block,
+                                       int32_t window) {
+  if (BH < 1 || N < 1 || window < 1 || block != kGpuBlock || (d != 64 && d != 128)) return 0;
+  const int64_t Nb = (int64_t(N) + block - 1) / block;
+  if (Nb > kMaxNb) return 0;
+  AttnProblem p{BH, N, d, block, int(Nb), 1.f};
+  return blade::gt_bwd_workspace_layout(p, int((int64_t(N) + window - 1) / window)).total;
+}
+
+blade_status_t blade_bsa_gt_bwd(const void* q, const void* k, const void* v, const void* kg,
+                                const void* vg, int32_t window, const void* o, const float* lse,
+                                const void* dout, int64_t BH, int32_t N, int32_t d,
+                                int32_t block, float scale, const int32_t* kv_idx,
+                                const int32_t* kv_cnt, void* dq, void* dk, void* dv,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  if (!q || !k || !v || !kg || !vg || !o || !lse || !dout || !kv_idx || !kv_cnt || !dq ||
+      !dk || !dv)
+    return BLADE_ERR_INVALID_ARG;
+  for (const void* x : {q, k, v, kg, vg, o, dout, static_cast<const void*>(dq),
+                        static_cast<const void*>(dk), static_cast<const void*>(dv)})
+    if (!aligned16(x)) return BLADE_ERR_INVALID_ARG;
+  if (BH < 1 || BH > 65535 || N < 1 || block < 1 || window < 1 || !(scale > 0.f) ||
+      !isfinite(scale))
+    return BLADE_ERR_INVALID_ARG;
+  if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  const int64_t Nb = (int64_t(N) + block - 1) / block;
+  if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
+  AttnProblem p{BH, N, d, block, int(Nb), scale};
+  const blade::GtProblem g{kg, vg, int((int64_t(N) + window - 1) / window), int(window)};
+  const size_t need = blade::gt_bwd_workspace_layout(p, g.Ng).total;
+  if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return BLADE_ERR_WORKSPACE;
+  cudaError_t e = blade::launch_attn_gt_bwd(p, g, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk,
+                                            dv, static_cast<char*>(workspace),
+                                            static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+
 const char* blade_status_string(blade_status_t status) {
   switch (status) {
     case BLADE_OK: return "ok";

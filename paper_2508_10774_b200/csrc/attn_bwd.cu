@@ -382,11 +382,266 @@ __global__ void __launch_bounds__(BW_THREADS) bsa_bwd_dq_kernel(
   store_rows<D>(dQ + base, q0 + warp * 16, N, lane, dq, scale);
 }
 
+// ---- ASA_GT backward (F1 + F3; oracle
+//      sparse_attention_gt_backward_unit).  With the forward's LSE taken over
+//      the kept keys AND the global tokens, P_rt = exp(s_rt - LSE_r) and D_r =
+//      dO_r . O_r already make the plain kernels above exact for the kept
+//      keys; the global tokens add, per window w (bias b_w = ln n_w):
+//        dVg_w = sum_r P_rw dO_r,  dKg_w = scale sum_r dS_rw q_r  (every query)
+//        dQ_r += scale sum_w dS_rw kg_w
+//      and MeanPool_n passes dKg_w / n_w, dVg_w / n_w to each token of w
+//      (the bf16 rounding of the pooled rows is the identity, R-24). ---------
+
+BLADE_DEVINL float gt_bias_log2(int w, int Ng, int N, int window) {
+  if (w >= Ng) return -INFINITY;  // padding rows / cols of the last 64-tile
+  return __logf(float(min(window, N - w * window))) * kLog2e;
+}
+
+// CTA = (64 global tokens g0.., head u, query-tile split s): dKg, dVg partial
+// sums over the split's 64-query tiles, fp32 to part[{0,1}][s][u][Ngp][D].
+template <int D>
+__global__ void __launch_bounds__(BW_THREADS) gt_bwd_dkdv_kernel(
+    const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Kg,
+    const __nv_bfloat16* __restrict__ Vg, const __nv_bfloat16* __restrict__ dO,
+    const float* __restrict__ LSE, const float* __restrict__ Dv, int N, int Ng, int window,
+    float scale, int tiles_per_split, int64_t part_stride, float* __restrict__ part) {
+  extern __shared__ __align__(128) char smem[];
+  constexpr int TB = BW_TILE * D * 2;
+  char* sK = smem;
+  char* sV = sK + TB;
+  char* sQ = sV + TB;        // [2]
+  char* sdO = sQ + 2 * TB;   // [2]
+  float* sL = reinterpret_cast<float*>(sdO + 2 * TB);
+  float* sD = sL + 2 * BW_TILE;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g0 = blockIdx.x * BW_ROWS;
+  const int64_t u = blockIdx.y;
+  const int s = blockIdx.z;
+  const int Ngp = gridDim.x * BW_ROWS;
+  const int nqt = (N + BW_TILE - 1) / BW_TILE;
+  const int t0 = s * tiles_per_split, t1 = min(nqt, t0 + tiles_per_split);
+  const int64_t base = u * int64_t(N) * D;
+  const int64_t gbase = u * int64_t(Ng) * D;
+  const float sl2 = scale * kLog2e;
+
+  load_tile<D>(smem_u32(sK), Kg + gbase, g0, Ng, tid);
+  load_tile<D>(smem_u32(sV), Vg + gbase, g0, Ng, tid);
+  auto load_q = [&](int t, int st) {
+    const int q0 = t * BW_TILE;
+    load_tile<D>(smem_u32(sQ + st * TB), Q + base, q0, N, tid);
+    load_tile<D>(smem_u32(sdO + st * TB), dO + base, q0, N, tid);
+    if (tid < BW_TILE) {
+      const int r = q0 + tid;
+      sL[st * BW_TILE + tid] = r < N ? LSE[u * N + r] * kLog2e : INFINITY;
+      sD[st * BW_TILE + tid] = r < N ? Dv[u * N + r] : 0.f;
+    }
+  };
+  if (t0 < t1) load_q(t0, 0);
+  cp_async_commit();
+
+  float dk[D / 8][4], dv[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
+  const int g = lane >> 2, qd = lane & 3;
+  const float b0 = gt_bias_log2(g0 + warp * 16 + g, Ng, N, window);
+  const float b1 = gt_bias_log2(g0 + warp * 16 + g + 8, Ng, N, window);
+
+  for (int t = t0; t < t1; ++t) {
+    const int st = (t - t0) & 1;
+    if (t + 1 < t1) load_q(t + 1, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const uint32_t q_t = smem_u32(sQ + st * TB), do_t = smem_u32(sdO + st * TB);
+    const float* L = sL + st * BW_TILE;
+    const float* Dd = sD + st * BW_TILE;
+    float p[8][4];
+    {
+      uint32_t ka[D / 16][4];
+      load_a_rows<D>(smem_u32(sK), warp * 16, lane, ka);
+      mma_rows_x_tileT<D>(ka, q_t, lane, p);
+    }
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float l0 = L[n * 8 + qd * 2], l1 = L[n * 8 + qd * 2 + 1];
+      p[n][0] = ex2(fmaf(p[n][0], sl2, b0 - l0));
+      p[n][1] = ex2(fmaf(p[n][1], sl2, b0 - l1));
+      p[n][2] = ex2(fmaf(p[n][2], sl2, b1 - l0));
+      p[n][3] = ex2(fmaf(p[n][3], sl2, b1 - l1));
+    }
+    mma_p_x_tile<D>(p, do_t, lane, dv);
+    float ds[8][4];
+    {
+      uint32_t va[D / 16][4];
+      load_a_rows<D>(smem_u32(sV), warp * 16, lane, va);
+      mma_rows_x_tileT<D>(va, do_t, lane, ds);
+    }
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float d0 = Dd[n * 8 + qd * 2], d1 = Dd[n * 8 + qd * 2 + 1];
+      ds[n][0] = p[n][0] * (ds[n][0] - d0);
+      ds[n][1] = p[n][1] * (ds[n][1] - d1);
+      ds[n][2] = p[n][2] * (ds[n][2] - d0);
+      ds[n][3] = p[n][3] * (ds[n][3] - d1);
+    }
+    mma_p_x_tile<D>(ds, q_t, lane, dk);
+    __syncthreads();
+  }
+  float* pk = part + (int64_t(s) * gridDim.y + u) * Ngp * D;
+  float* pv = pk + part_stride;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = g0 + warp * 16 + g + 8 * h;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      *reinterpret_cast<float2*>(pk + int64_t(r) * D + n * 8 + qd * 2) =
+          make_float2(dk[n][2 * h] * scale, dk[n][2 * h + 1] * scale);
+      *reinterpret_cast<float2*>(pv + int64_t(r) * D + n * 8 + qd * 2) =
+          make_float2(dv[n][2 * h], dv[n][2 * h + 1]);
+    }
+  }
+}
+
+// dKg/dVg (sum over the splits) / n_w, fp32 [2][BH][Ng][D]
+__global__ void gt_bwd_reduce_kernel(const float* __restrict__ part, int64_t part_stride,
+                                     int splits, int64_t BH, int Ng, int Ngp, int D, int N,
+                                     int window, float* __restrict__ g_out) {
+  const int64_t per = BH * Ng * D;
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= 2 * per) return;
+  const int which = int(e / per);
+  const int64_t r = e % per;
+  const int c = int(r % D);
+  const int w = int((r / D) % Ng);
+  const int64_t u = r / (int64_t(D) * Ng);
+  const float* src = part + which * part_stride + (u * Ngp + w) * D + c;
+  float acc = 0.f;
+  for (int s = 0; s < splits; ++s) acc += src[int64_t(s) * BH * Ngp * D];
+  g_out[e] = acc / float(min(window, N - w * window));
+}
+
+// dK[t] += dKg[w(t)] / n_w, dV likewise (bf16 read-modify-write, 8 per thread)
+__global__ void gt_bwd_unpool_kernel(const float* __restrict__ gsum, int64_t BH, int N, int Ng,
+                                     int D, int window, __nv_bfloat16* __restrict__ dK,
+                                     __nv_bfloat16* __restrict__ dV) {
+  const int64_t per8 = BH * N * D / 8;
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= 2 * per8) return;
+  const int which = int(e / per8);
+  const int64_t r = (e % per8) * 8;
+  const int c = int(r % D);
+  const int t = int((r / D) % N);
+  const int64_t u = r / (int64_t(D) * N);
+  const float* src = gsum + which * BH * Ng * D + (u * Ng + t / window) * D + c;
+  __nv_bfloat16* dst = (which ? dV : dK) + r;
+  uint4 raw = *reinterpret_cast<const uint4*>(dst);
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+  const float4 a = *reinterpret_cast<const float4*>(src);
+  const float4 b = *reinterpret_cast<const float4*>(src + 4);
+  const float add[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    h[i] = __floats2bfloat162_rn(f.x + add[2 * i], f.y + add[2 * i + 1]);
+  }
+  *reinterpret_cast<uint4*>(dst) = raw;
+}
+
+// CTA = 64 queries: dQ_r += scale sum_w dS_rw kg_w over all global tokens
+template <int D>
+__global__ void __launch_bounds__(BW_THREADS) gt_bwd_dq_kernel(
+    const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Kg,
+    const __nv_bfloat16* __restrict__ Vg, const __nv_bfloat16* __restrict__ dO,
+    const float* __restrict__ LSE, const float* __restrict__ Dv, int N, int Ng, int window,
+    float scale, __nv_bfloat16* __restrict__ dQ) {
+  extern __shared__ __align__(128) char smem[];
+  constexpr int TB = BW_TILE * D * 2;
+  char* sQ = smem;
+  char* sdO = sQ + TB;
+  char* sK = sdO + TB;       // [2]
+  char* sV = sK + 2 * TB;    // [2]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q0 = blockIdx.x * BW_ROWS;
+  const int64_t u = blockIdx.y;
+  const int64_t base = u * int64_t(N) * D;
+  const int64_t gbase = u * int64_t(Ng) * D;
+  const int ntiles = (Ng + BW_TILE - 1) / BW_TILE;
+  const float sl2 = scale * kLog2e;
+
+  load_tile<D>(smem_u32(sQ), Q + base, q0, N, tid);
+  load_tile<D>(smem_u32(sdO), dO + base, q0, N, tid);
+  auto load_kv = [&](int t, int st) {
+    load_tile<D>(smem_u32(sK + st * TB), Kg + gbase, t * BW_TILE, Ng, tid);
+    load_tile<D>(smem_u32(sV + st * TB), Vg + gbase, t * BW_TILE, Ng, tid);
+  };
+  load_kv(0, 0);
+  cp_async_commit();
+
+  const int g = lane >> 2, qd = lane & 3;
+  float lse2[2], dr[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = q0 + warp * 16 + g + 8 * h;
+    lse2[h] = r < N ? LSE[u * N + r] * kLog2e : 0.f;
+    dr[h] = r < N ? Dv[u * N + r] : 0.f;
+  }
+  float dq[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) dq[n][0] = dq[n][1] = dq[n][2] = dq[n][3] = 0.f;
+  uint32_t qa[D / 16][4], doa[D / 16][4];
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int st = t & 1;
+    if (t + 1 < ntiles) load_kv(t + 1, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (t == 0) {
+      load_a_rows<D>(smem_u32(sQ), warp * 16, lane, qa);
+      load_a_rows<D>(smem_u32(sdO), warp * 16, lane, doa);
+    }
+    const uint32_t k_t = smem_u32(sK + st * TB), v_t = smem_u32(sV + st * TB);
+    float p[8][4], ds[8][4];
+    mma_rows_x_tileT<D>(qa, k_t, lane, p);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float bw = gt_bias_log2(t * BW_TILE + n * 8 + qd * 2 + (e & 1), Ng, N, window);
+        p[n][e] = ex2(fmaf(p[n][e], sl2, bw - lse2[e >> 1]));
+      }
+    }
+    mma_rows_x_tileT<D>(doa, v_t, lane, ds);
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ds[n][e] = p[n][e] * (ds[n][e] - dr[e >> 1]);
+    mma_p_x_tile<D>(ds, k_t, lane, dq);
+    __syncthreads();
+  }
+  // dQ (already holding the kept-key part) += scale * acc
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = q0 + warp * 16 + g + 8 * h;
+    if (r < N) {
+      __nv_bfloat16* row = dQ + base + int64_t(r) * D;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        __nv_bfloat162* x = reinterpret_cast<__nv_bfloat162*>(row + n * 8 + qd * 2);
+        const float2 f = __bfloat1622float2(*x);
+        *x = __floats2bfloat162_rn(f.x + dq[n][2 * h] * scale, f.y + dq[n][2 * h + 1] * scale);
+      }
+    }
+  }
+}
+
 template <int D>
 cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                          const void* o, const float* lse, const void* dout,
                          const int32_t* kv_idx, const int32_t* kv_cnt, void* dq, void* dk,
-                         void* dv, char* ws, cudaStream_t stream) {
+                         void* dv, char* ws, cudaStream_t stream, const GtProblem* gp) {
   const BwdWorkspace w = bwd_workspace_layout(p);
   float* Dvec = reinterpret_cast<float*>(ws + w.off_d);
   int32_t* q_idx = reinterpret_cast<int32_t*>(ws + w.off_qidx);
@@ -419,13 +674,56 @@ cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, con
         reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (gp) {  // dK_g, dV_g partials -> sums / n_w -> spread over the windows
+    const GtBwdWorkspace gw = gt_bwd_workspace_layout(p, gp->Ng);
+    float* part = reinterpret_cast<float*>(ws + gw.off_part);
+    float* gsum = reinterpret_cast<float*>(ws + gw.off_gsum);
+    const int64_t part_stride = int64_t(gw.splits) * p.BH * gw.Ngp * D;
+    bool done = false;
+#ifndef BLADE_BWD_DKDV_MMA_SYNC
+    e = launch_bwd_dkdv_tc(p, q, k, v, lse, dout, Dvec, nullptr, nullptr, nullptr, nullptr,
+                           stream, gp, part, gw.splits);
+    if (e != cudaSuccess && e != cudaErrorNotSupported) return e;
+    done = e == cudaSuccess;
+#endif
+    if (!done) {
+      e = cudaFuncSetAttribute(gt_bwd_dkdv_kernel<D>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
+      if (e != cudaSuccess) return e;
+      const int nqt = (p.N + BW_TILE - 1) / BW_TILE;
+      const int tps = (nqt + gw.splits - 1) / gw.splits;
+      gt_bwd_dkdv_kernel<D><<<dim3(unsigned(gw.Ngp / BW_ROWS), unsigned(p.BH),
+                                   unsigned(gw.splits)),
+                              BW_THREADS, smem_kv, stream>>>(
+          B(q), B(gp->kg), B(gp->vg), B(dout), lse, Dvec, p.N, gp->Ng, gp->window, p.scale, tps,
+          part_stride, part);
+    }
+    const int64_t nred = 2 * p.BH * gp->Ng * D;
+    gt_bwd_reduce_kernel<<<unsigned((nred + 255) / 256), 256, 0, stream>>>(
+        part, part_stride, gw.splits, p.BH, gp->Ng, gw.Ngp, D, p.N, gp->window, gsum);
+    const int64_t nun = 2 * p.BH * p.N * D / 8;
+    gt_bwd_unpool_kernel<<<unsigned((nun + 255) / 256), 256, 0, stream>>>(
+        gsum, p.BH, p.N, gp->Ng, D, gp->window, reinterpret_cast<__nv_bfloat16*>(dk),
+        reinterpret_cast<__nv_bfloat16*>(dv));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
 #ifndef BLADE_BWD_DQ_MMA_SYNC
-  e = launch_bwd_dq_tc(p, q, k, v, lse, dout, Dvec, kv_idx, kv_cnt, dq, stream);
+  e = launch_bwd_dq_tc(p, q, k, v, lse, dout, Dvec, kv_idx, kv_cnt, dq, stream, gp);
   if (e != cudaErrorNotSupported) return e;
 #endif
   bsa_bwd_dq_kernel<D><<<grid, BW_THREADS, smem_q, stream>>>(
       B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, kv_idx, kv_cnt,
       reinterpret_cast<__nv_bfloat16*>(dq));
+  if (gp) {  // + the global tokens' share of dQ (read-modify-write)
+    e = cudaFuncSetAttribute(gt_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_q);
+    if (e != cudaSuccess) return e;
+    gt_bwd_dq_kernel<D><<<dim3(unsigned((p.N + BW_ROWS - 1) / BW_ROWS), unsigned(p.BH)),
+                          BW_THREADS, smem_q, stream>>>(
+        B(q), B(gp->kg), B(gp->vg), B(dout), lse, Dvec, p.N, gp->Ng, gp->window, p.scale,
+        reinterpret_cast<__nv_bfloat16*>(dq));
+  }
   return cudaGetLastError();
 }
 
@@ -436,9 +734,23 @@ cudaError_t launch_attn_bwd(const AttnProblem& p, const void* q, const void* k, 
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* dq, void* dk,
                             void* dv, char* ws, cudaStream_t stream) {
   if (p.d == 64)
-    return launch_bwd_d<64>(p, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk, dv, ws, stream);
+    return launch_bwd_d<64>(p, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk, dv, ws, stream,
+                            nullptr);
   if (p.d == 128)
-    return launch_bwd_d<128>(p, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk, dv, ws, stream);
+    return launch_bwd_d<128>(p, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk, dv, ws, stream,
+                             nullptr);
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_attn_gt_bwd(const AttnProblem& p, const GtProblem& gp, const void* q,
+                               const void* k, const void* v, const void* o, const float* lse,
+                               const void* dout, const int32_t* kv_idx, const int32_t* kv_cnt,
+                               void* dq, void* dk, void* dv, char* ws, cudaStream_t stream) {
+  if (p.d == 64)
+    return launch_bwd_d<64>(p, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk, dv, ws, stream, &gp);
+  if (p.d == 128)
+    return launch_bwd_d<128>(p, q, k, v, o, lse, dout, kv_idx, kv_cnt, dq, dk, dv, ws, stream,
+                             &gp);
   return cudaErrorNotSupported;
 }
 

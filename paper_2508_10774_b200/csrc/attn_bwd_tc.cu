@@ -50,10 +50,26 @@ struct BCfg {
 
 constexpr int kBThreads = 224;
 
-template <int D>
+// ASA_GT (attn_bwd.cu header): the global tokens as extra 128-row items.
+struct BwdGtArgs {
+  int Ng = 0, ngt = 0;        // global tokens, 128-row tiles of them
+  float bfull2 = 0.f, blast2 = 0.f;  // ln(n) log2e, ln(n_last) log2e
+  int qps = 0;                // dK/dV of the global tokens: query blocks per split
+  float* part = nullptr;      // fp32 partials [2][splits][BH][ngt*128][D]
+  int64_t part_stride = 0;    // floats between the dK and dV partials
+};
+
+// log2-domain bias of global token w (-inf past N_g: P = 0)
+BLADE_DEVINL float gt_bias2(const BwdGtArgs& g, int w) {
+  return w < g.Ng - 1 ? g.bfull2 : (w == g.Ng - 1 ? g.blast2 : -INFINITY);
+}
+
+template <int D, bool kGT>
 __global__ void __launch_bounds__(kBThreads, 1)
     bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                     const __grid_constant__ CUtensorMap tmKg,
+                     const __grid_constant__ CUtensorMap tmVg, const BwdGtArgs gt,
                      int N, int Nb, float scale, const float* __restrict__ LSE,
                      const float* __restrict__ Dv, const int32_t* __restrict__ kv_idx,
                      const int32_t* __restrict__ kv_cnt, __nv_bfloat16* __restrict__ dQ) {
@@ -82,6 +98,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int64_t u = blockIdx.y;
   const int cnt = kv_cnt[u * Nb + i];
   const int32_t* list = kv_idx + (u * Nb + i) * Nb;
+  const int total = cnt + (kGT ? gt.ngt : 0);  // kept blocks, then global-token tiles
 
   if (warp == 5 && lane == 0) {
     tc::mbar_init(bar_q, 1);
@@ -126,11 +143,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
       char* ring = isK ? sRingK : sRingV;
       uint64_t* full = isK ? bar_kfull : bar_vfull;
       uint64_t* empty = isK ? bar_kempty : bar_vempty;
-      const CUtensorMap* m = isK ? &tmK : &tmV;
       int jn = cnt > 0 ? __ldg(list) : 0;
-      for (int n = 0; n < cnt; ++n) {
-        const int jb = jn;
+      for (int n = 0; n < total; ++n) {
+        const int jb = n < cnt ? jn : n - cnt;
         if (n + 1 < cnt) jn = __ldg(list + n + 1);
+        const CUtensorMap* m = (kGT && n >= cnt) ? (isK ? &tmKg : &tmVg) : (isK ? &tmK : &tmV);
         const int s = n % R;
         tc::mbar_wait(empty + s, ((n / R) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(full + s, C::kTile);
@@ -141,7 +158,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
   } else if (warp == 4) {
     // ===================== MMA issuer =====================
-    if (lane == 0 && cnt > 0) {
+    if (lane == 0 && total > 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idQ = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t qa = smem_u32(sQ), da = smem_u32(sDO);
@@ -173,8 +190,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
       };
       issue_S(0);
       issue_dP(0);
-      for (int n = 0; n < cnt; ++n) {
-        if (n + 1 < cnt) {
+      for (int n = 0; n < total; ++n) {
+        if (n + 1 < total) {
           tc::mbar_wait(bar_sf, n & 1);  // S(n) is in registers: its columns are free
           issue_S(n + 1);
         }
@@ -188,9 +205,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
                      (n > 0 || ks > 0) ? 1 : 0);
         tc::commit(bar_dq);
         tc::commit(bar_kempty + (n % C::kRingK));
-        if (n + 1 < cnt) issue_dP(n + 1);
+        if (n + 1 < total) issue_dP(n + 1);
       }
-      tc::mbar_wait(bar_dq, (cnt - 1) & 1);
+      tc::mbar_wait(bar_dq, (total - 1) & 1);
     }
   } else if (warp < 4) {
     // ===================== elementwise: P, dS =====================
@@ -201,7 +218,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const float lse2 = row < N ? LSE[u * N + row] * kLog2e : INFINITY;  // P = 0 past N
     const float dr = row < N ? Dv[u * N + row] : 0.f;
     int jn = cnt > 0 ? __ldg(list) : 0;
-    for (int n = 0; n < cnt; ++n) {
+    for (int n = 0; n < total; ++n) {
       const int jb = jn;
       if (n + 1 < cnt) jn = __ldg(list + n + 1);
       tc::mbar_wait(bar_sc, n & 1);
@@ -218,13 +235,19 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bar_sf);
-      const int valid = N - jb * 128;  // keys of a partial last block
+      if (!kGT || n < cnt) {
+        const int valid = N - jb * 128;  // keys of a partial last block
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
-                              make_float2(-lse2, -lse2));
-        p[c] = c < valid ? ex2(x.x) : 0.f;
-        p[c + 1] = c + 1 < valid ? ex2(x.y) : 0.f;
+        for (int c = 0; c < 128; c += 2) {
+          const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
+                                make_float2(-lse2, -lse2));
+          p[c] = c < valid ? ex2(x.x) : 0.f;
+          p[c + 1] = c + 1 < valid ? ex2(x.y) : 0.f;
+        }
+      } else {  // global tokens w0 + c: + ln n_w
+        const int w0 = (n - cnt) * 128;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) p[c] = ex2(fmaf(p[c], sl2, gt_bias2(gt, w0 + c) - lse2));
       }
       tc::mbar_wait(bar_dp, n & 1);
       tc::fence_after_sync();
@@ -250,12 +273,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
       if (lane == 0) tc::mbar_arrive(bar_ds);
     }
     // epilogue: dQ * scale -> bf16
-    if (cnt > 0) {
-      tc::mbar_wait(bar_dq, (cnt - 1) & 1);
+    if (total > 0) {
+      tc::mbar_wait(bar_dq, (total - 1) & 1);
       tc::fence_after_sync();
     }
     __nv_bfloat16* out = dQ + (u * N + row) * int64_t(D);
-    if (cnt == 0) {  // no kept block (never produced by blade_asa_mask): dQ = 0
+    if (total == 0) {  // no kept block (never produced by blade_asa_mask): dQ = 0
       if (row < N)
         for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
     } else
@@ -314,11 +337,15 @@ struct KCfg {
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D;
 };
 
-template <int D>
+// kGT: the "key block" j is a 128-row tile of global tokens (tmK/tmV map
+// K_g/V_g), every query block attends it, blockIdx.z splits the query blocks
+// (gt.qps each) and the sums go to fp32 partials gt.part (attn_bwd.cu reduces
+// them and spreads dK_g/n_w, dV_g/n_w over the windows).
+template <int D, bool kGT>
 __global__ void __launch_bounds__(kBThreads, 1)
     bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                        const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                       int N, int Nb, float scale, const float* __restrict__ LSE,
+                       const BwdGtArgs gt, int N, int Nb, float scale, const float* __restrict__ LSE,
                        const float* __restrict__ Dv, const int32_t* __restrict__ q_idx,
                        const int32_t* __restrict__ q_cnt, __nv_bfloat16* __restrict__ dK,
                        __nv_bfloat16* __restrict__ dV) {
@@ -343,8 +370,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j = blockIdx.x;
   const int64_t u = blockIdx.y;
-  const int cnt = q_cnt[u * Nb + j];
-  const int32_t* list = q_idx + (u * Nb + j) * Nb;
+  const int i_first = kGT ? int(blockIdx.z) * gt.qps : 0;
+  const int cnt = kGT ? max(0, min(Nb, i_first + gt.qps) - i_first) : q_cnt[u * Nb + j];
+  const int32_t* list = kGT ? nullptr : q_idx + (u * Nb + j) * Nb;
+  auto qblock = [&](int n) { return kGT ? i_first + n : __ldg(list + n); };
 
   if (warp == 5 && lane == 0) {
     tc::mbar_init(bar_kv, 1);
@@ -375,10 +404,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
         tc::tma_load_3d(sK + p * C::kPanel, &tmK, bar_kv, p * 64, j * 128, int(u));
         tc::tma_load_3d(sV + p * C::kPanel, &tmV, bar_kv, p * 64, j * 128, int(u));
       }
-      int in = cnt > 0 ? __ldg(list) : 0;
+      int in = cnt > 0 ? qblock(0) : 0;
       for (int n = 0; n < cnt; ++n) {
         const int ib = in;
-        if (n + 1 < cnt) in = __ldg(list + n + 1);
+        if (n + 1 < cnt) in = qblock(n + 1);
         const int s = n % C::kRing;
         tc::mbar_wait(bar_empty + s, ((n / C::kRing) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(bar_full + s, 2 * C::kTile);
@@ -448,10 +477,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
     const int r = warp * 32 + lane;
     const float sl2 = scale * kLog2e;
-    int in = cnt > 0 ? __ldg(list) : 0;
+    const float brow = kGT ? gt_bias2(gt, j * 128 + r) : 0.f;  // ln n_w of this key row
+    int in = cnt > 0 ? qblock(0) : 0;
     for (int n = 0; n < cnt; ++n) {
       const int ib = in;
-      if (n + 1 < cnt) in = __ldg(list + n + 1);
+      if (n + 1 < cnt) in = qblock(n + 1);
       float* L = sLD + (n & 1) * 256;
       {  // stage LSE_i (log2 domain) and D_i: query column r
         const int qrow = ib * 128 + r;
@@ -473,7 +503,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #pragma unroll
       for (int c = 0; c < 128; c += 2) {
         const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
-                              make_float2(-L[c], -L[c + 1]));
+                              kGT ? make_float2(brow - L[c], brow - L[c + 1])
+                                  : make_float2(-L[c], -L[c + 1]));
         p[c] = ex2(x.x);
         p[c + 1] = ex2(x.y);
       }
@@ -516,6 +547,31 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tc::fence_after_sync();
     }
     const int krow = j * 128 + r;
+    if constexpr (kGT) {  // fp32 partials (dK_g scaled), every row of the tile
+      const int Ngp = gt.ngt * 128;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        float* out = gt.part + which * gt.part_stride +
+                     ((int64_t(blockIdx.z) * gridDim.y + u) * Ngp + krow) * int64_t(D);
+        const float z = which ? 1.f : scale;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t rr[32];
+          if (cnt > 0) {
+            tc::ld_32x32b_x32(tmem + lane_base + (which ? C::kColDV : C::kColDK) + c * 32, rr);
+            tc::wait_ld();
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            *reinterpret_cast<float4*>(out + c * 32 + 4 * e) =
+                cnt > 0 ? make_float4(__uint_as_float(rr[4 * e]) * z,
+                                      __uint_as_float(rr[4 * e + 1]) * z,
+                                      __uint_as_float(rr[4 * e + 2]) * z,
+                                      __uint_as_float(rr[4 * e + 3]) * z)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    } else
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       __nv_bfloat16* out = (which ? dV : dK) + (u * N + krow) * int64_t(D);
@@ -556,18 +612,30 @@ template <int D>
 cudaError_t launch_dkdv_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                           const float* lse, const void* dout, const float* Dv,
                           const int32_t* q_idx, const int32_t* q_cnt, void* dk, void* dv,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const GtProblem* g, float* part, int splits) {
   CUtensorMap mq, mdo, mk, mv;
+  const int64_t krows = g ? g->Ng : p.N;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mdo, dout, p.BH, p.N, D) ||
-      !make_tile_map(&mk, k, p.BH, p.N, D) || !make_tile_map(&mv, v, p.BH, p.N, D))
+      !make_tile_map(&mk, g ? g->kg : k, p.BH, krows, D) ||
+      !make_tile_map(&mv, g ? g->vg : v, p.BH, krows, D))
     return cudaErrorNotSupported;
   constexpr int smem = KCfg<D>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(bwd_dkdv_tc_kernel<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  BwdGtArgs ga{};
+  if (g) {
+    ga.Ng = g->Ng;
+    ga.ngt = (g->Ng + 127) / 128;
+    ga.bfull2 = logf(float(g->window)) * kLog2e;
+    ga.blast2 = logf(float(p.N - (g->Ng - 1) * g->window)) * kLog2e;
+    ga.qps = (p.Nb + splits - 1) / splits;
+    ga.part = part;
+    ga.part_stride = int64_t(splits) * p.BH * ga.ngt * 128 * D;
+  }
+  auto kern = g ? bwd_dkdv_tc_kernel<D, true> : bwd_dkdv_tc_kernel<D, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(unsigned(p.Nb), unsigned(p.BH));
-  bwd_dkdv_tc_kernel<D><<<grid, kBThreads, smem, stream>>>(
-      mq, mdo, mk, mv, p.N, p.Nb, p.scale, lse, Dv, q_idx, q_cnt,
+  dim3 grid(unsigned(g ? ga.ngt : p.Nb), unsigned(p.BH), unsigned(g ? splits : 1));
+  kern<<<grid, kBThreads, smem, stream>>>(
+      mq, mdo, mk, mv, ga, p.N, p.Nb, p.scale, lse, Dv, q_idx, q_cnt,
       reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
   return cudaGetLastError();
 }
@@ -576,19 +644,31 @@ template <int D>
 cudaError_t launch_dq_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                         const float* lse, const void* dout, const float* Dv,
                         const int32_t* kv_idx, const int32_t* kv_cnt, void* dq,
-                        cudaStream_t stream) {
-  CUtensorMap mq, mdo, mk, mv;
+                        cudaStream_t stream, const GtProblem* g) {
+  CUtensorMap mq, mdo, mk, mv, mkg, mvg;
   if (!make_tile_map(&mq, q, p.BH, p.N, D) || !make_tile_map(&mdo, dout, p.BH, p.N, D) ||
       !make_tile_map(&mk, k, p.BH, p.N, D) || !make_tile_map(&mv, v, p.BH, p.N, D))
     return cudaErrorNotSupported;
+  BwdGtArgs ga{};
+  if (g) {
+    if (!make_tile_map(&mkg, g->kg, p.BH, g->Ng, D) || !make_tile_map(&mvg, g->vg, p.BH, g->Ng, D))
+      return cudaErrorNotSupported;
+    ga.Ng = g->Ng;
+    ga.ngt = (g->Ng + 127) / 128;
+    ga.bfull2 = logf(float(g->window)) * kLog2e;
+    ga.blast2 = logf(float(p.N - (g->Ng - 1) * g->window)) * kLog2e;
+  } else {
+    mkg = mk;
+    mvg = mv;
+  }
   constexpr int smem = BCfg<D>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(bwd_dq_tc_kernel<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kern = g ? bwd_dq_tc_kernel<D, true> : bwd_dq_tc_kernel<D, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(p.Nb), unsigned(p.BH));
-  bwd_dq_tc_kernel<D><<<grid, kBThreads, smem, stream>>>(mq, mdo, mk, mv, p.N, p.Nb, p.scale, lse,
-                                                          Dv, kv_idx, kv_cnt,
-                                                          reinterpret_cast<__nv_bfloat16*>(dq));
+  kern<<<grid, kBThreads, smem, stream>>>(mq, mdo, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale, lse,
+                                          Dv, kv_idx, kv_cnt,
+                                          reinterpret_cast<__nv_bfloat16*>(dq));
   return cudaGetLastError();
 }
 
@@ -597,20 +677,25 @@ cudaError_t launch_dq_d(const AttnProblem& p, const void* q, const void* k, cons
 cudaError_t launch_bwd_dkdv_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                                const float* lse, const void* dout, const float* Dv,
                                const int32_t* q_idx, const int32_t* q_cnt, void* dk, void* dv,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, const GtProblem* gt, float* part,
+                               int splits) {
   if (p.d == 64)
-    return launch_dkdv_d<64>(p, q, k, v, lse, dout, Dv, q_idx, q_cnt, dk, dv, stream);
+    return launch_dkdv_d<64>(p, q, k, v, lse, dout, Dv, q_idx, q_cnt, dk, dv, stream, gt, part,
+                             splits);
   if (p.d == 128)
-    return launch_dkdv_d<128>(p, q, k, v, lse, dout, Dv, q_idx, q_cnt, dk, dv, stream);
+    return launch_dkdv_d<128>(p, q, k, v, lse, dout, Dv, q_idx, q_cnt, dk, dv, stream, gt, part,
+                              splits);
   return cudaErrorNotSupported;
 }
 
 cudaError_t launch_bwd_dq_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                              const float* lse, const void* dout, const float* Dv,
                              const int32_t* kv_idx, const int32_t* kv_cnt, void* dq,
-                             cudaStream_t stream) {
-  if (p.d == 64) return launch_dq_d<64>(p, q, k, v, lse, dout, Dv, kv_idx, kv_cnt, dq, stream);
-  if (p.d == 128) return launch_dq_d<128>(p, q, k, v, lse, dout, Dv, kv_idx, kv_cnt, dq, stream);
+                             cudaStream_t stream, const GtProblem* gt) {
+  if (p.d == 64)
+    return launch_dq_d<64>(p, q, k, v, lse, dout, Dv, kv_idx, kv_cnt, dq, stream, gt);
+  if (p.d == 128)
+    return launch_dq_d<128>(p, q, k, v, lse, dout, Dv, kv_idx, kv_cnt, dq, stream, gt);
   return cudaErrorNotSupported;
 }
 

@@ -134,16 +134,45 @@ cudaError_t launch_attn_bwd(const AttnProblem& p, const void* q, const void* k, 
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* dq, void* dk,
                             void* dv, char* ws, cudaStream_t stream);
 
+// ASA_GT backward (attn_bwd.cu): the plain backward's workspace, then the
+// global tokens' fp32 partial sums part [2][splits][BH][Ngp][d] (the query
+// blocks split so the grid covers the SMs) and their reduction gsum [2][BH][Ng][d].
+struct GtBwdWorkspace {
+  int splits, Ngp;
+  size_t off_part, off_gsum, total;
+};
+inline GtBwdWorkspace gt_bwd_workspace_layout(const AttnProblem& p, int Ng) {
+  GtBwdWorkspace w{};
+  w.Ngp = (Ng + 127) / 128 * 128;  // whole 128-row tiles (tcgen05 kernel; 64 for mma.sync)
+  const int64_t ctas = p.BH * (w.Ngp / 128);  // one CTA per SM: about four waves
+  int s = int((4 * 148 + ctas - 1) / ctas);
+  s = s < 1 ? 1 : (s > 64 ? 64 : s);
+  w.splits = s > p.Nb ? p.Nb : s;
+  size_t o = bwd_workspace_layout(p).total;
+  w.off_part = o; o = align256(o + 2 * size_t(w.splits) * p.BH * w.Ngp * p.d * 4);
+  w.off_gsum = o; o = align256(o + 2 * size_t(p.BH) * Ng * p.d * 4);
+  w.total = o;
+  return w;
+}
+cudaError_t launch_attn_gt_bwd(const AttnProblem& p, const GtProblem& gp, const void* q,
+                               const void* k, const void* v, const void* o, const float* lse,
+                               const void* dout, const int32_t* kv_idx, const int32_t* kv_cnt,
+                               void* dq, void* dk, void* dv, char* ws, cudaStream_t stream);
+
 // dQ of the backward on tcgen05 (attn_bwd_tc.cu); cudaErrorNotSupported if the
 // tensor maps cannot be built.
+// gt != nullptr: dK/dV of the global tokens (K_g/V_g tiles against every
+// query block, `splits` query ranges) into fp32 partials `part` laid out as
+// GtBwdWorkspace; dQ with the global-token tiles appended to every list.
 cudaError_t launch_bwd_dkdv_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                                const float* lse, const void* dout, const float* Dv,
                                const int32_t* q_idx, const int32_t* q_cnt, void* dk, void* dv,
-                               cudaStream_t stream);
+                               cudaStream_t stream, const GtProblem* gt = nullptr,
+                               float* part = nullptr, int splits = 1);
 cudaError_t launch_bwd_dq_tc(const AttnProblem& p, const void* q, const void* k, const void* v,
                              const float* lse, const void* dout, const float* Dv,
                              const int32_t* kv_idx, const int32_t* kv_cnt, void* dq,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const GtProblem* gt = nullptr);
 
 // One query block per CTA, three S buffers in TMEM (attn_tc3.cu).
 cudaError_t launch_attn_tc3(const AttnProblem& p, const void* q, const void* k, const void* v,

@@ -99,3 +99,45 @@ def test_backward_deterministic(A):
     torch.cuda.synchronize()
     for a, b in zip(g1, g2):
         assert torch.equal(a, b)
+
+
+GT_CASES = [(1, 512, 64, 0.5, 128), (2, 300, 128, 0.6, 100), (1, 1000, 128, 0.3, 7),
+            (2, 129, 64, 1.0, 128), (1, 2048, 128, 0.2, 128), (1, 70, 64, 1.0, 1000)]
+
+
+@pytest.mark.parametrize("case", GT_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_gt_backward_parity_given_mask(A, case):
+    """ASA_GT backward (F1 + F3) vs the oracle, same bounds as above; window
+    sizes span full, ragged, tiny (n = 7: N_g = 143 spans three 64-row tiles)
+    and larger than N (one global token)."""
+    BH, N, d, density, n = case
+    q, k, v = inputs.iid(1, BH, N, d, seed=N + d + 3)
+    do = inputs.iid(1, BH, N, d, seed=N + d + 4)[0]
+    Nb = O.num_blocks(N, 128)
+    kv_idx, kv_cnt = _lists(BH, Nb, np.random.default_rng(N + 1), density)
+    qd, kd, vd, dod = PT.to_dev(q, k, v, do)
+    ki, kc = PT.lists_to_dev(kv_idx, kv_cnt)
+    kg, vg = A.blade_gt_pool(kd, vd, window=n)
+    o, lse = A.blade_bsa_gt_fwd(qd, kd, vd, ki, kc, kg, vg, window=n)
+    dq, dk, dv = A.blade_bsa_gt_bwd(qd, kd, vd, kg, vg, o, lse, dod, ki, kc, window=n)
+    g2 = A.blade_bsa_gt_bwd(qd, kd, vd, kg, vg, o, lse, dod, ki, kc, window=n)
+    torch.cuda.synchronize()
+    for a, b in zip((dq, dk, dv), g2):
+        assert torch.equal(a, b)  # deterministic
+    rq, rk, rv = O.sparse_attention_gt_backward(q, k, v, do, kv_idx, kv_cnt, 128, n)
+    for got, ref, nm in ((dq, rq, "dq"), (dk, rk, "dk"), (dv, rv, "dv")):
+        _check(got, ref, nm)
+
+
+def test_gt_backward_smooth_end_to_end(A):
+    q, k, v = inputs.smooth(1, 2, 1500, 128, (1, 1, 1500), ell=3.0, beta=9.0, seed=3)
+    do = inputs.iid(1, 2, 1500, 128, seed=8)[0]
+    qd, kd, vd, dod = PT.to_dev(q, k, v, do)
+    o, lse, m = A.asa_gt_forward(qd, kd, vd, window=128, tau=0.9)
+    kg, vg = A.blade_gt_pool(kd, vd, window=128)
+    dq, dk, dv = A.blade_bsa_gt_bwd(qd, kd, vd, kg, vg, o, lse, dod, m.kv_idx, m.kv_cnt)
+    torch.cuda.synchronize()
+    rq, rk, rv = O.sparse_attention_gt_backward(q, k, v, do, m.kv_idx.cpu().numpy(),
+                                                m.kv_cnt.cpu().numpy(), 128, 128)
+    for got, ref, nm in ((dq, rq, "dq"), (dk, rk, "dk"), (dv, rv, "dv")):
+        _check(got, ref, nm)
