@@ -45,6 +45,8 @@ def main():
     copies = {"bench_wan.json": "bench_wan.json", "bench_cog.json": "bench_cog.json",
               "bench_wan_gt.json": "bench_wan_asa_gt.json", "bench_ref.json": "bench_reference_arm.json",
               "bench_bwd_wan.json": "bench_bwd_wan.json", "bench_bwd_cog.json": "bench_bwd_cog.json",
+              "bench_bwd_wan_asa_gt.json": "bench_bwd_wan_asa_gt.json",
+              "bench_bwd_cog_asa_gt.json": "bench_bwd_cog_asa_gt.json",
               "launches_wan.csv": "launches_wan_keep51.csv", "launches_cog.csv": "launches_cog_keep25.csv",
               "launches_bwd_wan.csv": "launches_bwd_wan.csv", "sweep_wan.jsonl": "sweep_wan.jsonl",
               "pytest_gpu.log": "pytest_gpu.log", "smoke.log": "smoke.log"}

@@ -5,6 +5,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/prof
 bash scripts/gpu_profile_round.sh
 python scripts/bench_bwd.py > gpurun_out/prof/bench_bwd_wan.json 2>&1
 python scripts/bench_bwd.py --workload cog > gpurun_out/prof/bench_bwd_cog.json 2>&1
+python scripts/bench_bwd.py --variant asa_gt > gpurun_out/prof/bench_bwd_wan_asa_gt.json 2>&1
+python scripts/bench_bwd.py --workload cog --variant asa_gt > gpurun_out/prof/bench_bwd_cog_asa_gt.json 2>&1
 python scripts/sweep.py --steps 10 > gpurun_out/prof/sweep_wan.jsonl 2>/dev/null
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:bwd -c 8 --csv --log-file gpurun_out/prof/launches_bwd_wan.csv python scripts/bench_bwd.py --steps 1 > /dev/null 2>&1
 cat gpurun_out/prof/pytest_gpu.log gpurun_out/prof/smoke.log
