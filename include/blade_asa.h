@@ -104,7 +104,7 @@ blade_status_t blade_asa_mask(const void* q, const void* k, int64_t BH, int32_t 
 size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block);
 
 /* Attention implementations (the `impl` argument of blade_bsa_fwd). */
-#define BLADE_ATTN_AUTO 0      /* fastest available: tcgen05/TMEM/TMA kernel          */
+#define BLADE_ATTN_AUTO 0      /* fastest measured: TCGEN05_PAIR for d = 64 and 128     */
 #define BLADE_ATTN_TCGEN05 1   /* sm_100a tcgen05 + TMEM + TMA warp-specialised kernel */
 #define BLADE_ATTN_MMA_SYNC 2  /* legacy mma.sync baseline (kept for comparison)       */
 #define BLADE_ATTN_TCGEN05_PAIR 3 /* tcgen05 kernel with two query blocks per CTA (ping-pong) */

@@ -116,9 +116,10 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
     return BLADE_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
-  // AUTO: the two-blocks-per-CTA kernel where it is faster on B200 (d = 64,
-  // Cog layer 1.03 vs 1.13 ms), the one-block kernel for d = 128 (1.19 vs 1.20)
-  const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64);
+  // AUTO: the two-blocks-per-CTA kernel, faster on B200 for both head dims
+  // (interleaved A/B: Cog d = 64 1.038 vs 1.232 ms; Wan d = 128 1.170-1.180 vs
+  // 1.181-1.189 ms, fused step 1.37-1.39 vs 1.40-1.43 ms)
+  const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || impl == BLADE_ATTN_AUTO;
   if (impl == BLADE_ATTN_MMA_SYNC) {
     e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
   } else if (pair) {
@@ -168,7 +169,7 @@ blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_
   // programmatic dependent launch of the attention behind K-mask.4 (tcgen05
   // kernels only): rows K-mask.4 recomputes carry a provisional negative
   // count, and only their CTAs wait for it (SURVEY F4 "fused mask->attention")
-  const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64);
+  const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || impl == BLADE_ATTN_AUTO;
   const bool pdl = impl == BLADE_ATTN_AUTO || impl == BLADE_ATTN_TCGEN05 || pair;
   mp.neg_flagged = pdl ? 1 : 0;
   // LPT order of the attention CTAs when the counts vary (lo < hi); in
@@ -235,7 +236,7 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
       impl == BLADE_ATTN_TCGEN05_TRIPLE
           ? blade::launch_attn_tc3(p, q, k, v, kv_idx, kv_cnt, o, lse,
                                    static_cast<cudaStream_t>(stream), &g)
-      : (impl == BLADE_ATTN_TCGEN05_PAIR || (impl == BLADE_ATTN_AUTO && d == 64))
+      : (impl == BLADE_ATTN_TCGEN05_PAIR || impl == BLADE_ATTN_AUTO)
           ? blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse,
                                    static_cast<cudaStream_t>(stream), &g)
           : blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,

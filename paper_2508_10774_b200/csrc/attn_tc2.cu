@@ -90,10 +90,15 @@ __device__ long long g_tr2[12][40];
   } while (0)
 #endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-#ifndef BLADE_ATTN2_EMU_MASK
-#define BLADE_ATTN2_EMU_MASK 0x11  // which of every 8 exponential pairs run on the FMA pipe
+// Which of every 8 exponential pairs run on the FMA pipe (ex2_poly2) instead
+// of MUFU: 1 in 8 for d = 64, none for d = 128 (interleaved A/B on B200:
+// Cog 1.038 ms vs 1.045 (1 in 4) / 1.046 (none); Wan 1.166-1.171 vs 1.176
+// (1 in 8) / 1.203-1.217 (1 in 4); 2 and 4 in 8 lose on both).
+#ifdef BLADE_ATTN2_EMU_MASK
+constexpr uint32_t kEmuMask2_64 = BLADE_ATTN2_EMU_MASK, kEmuMask2_128 = BLADE_ATTN2_EMU_MASK;
+#else
+constexpr uint32_t kEmuMask2_64 = 0x01, kEmuMask2_128 = 0x00;
 #endif
-constexpr uint32_t kEmuMask2 = BLADE_ATTN2_EMU_MASK;
 
 // Interleaved consumption order of the two blocks' items: A0 B0 A1 B1 ...
 // (when one list is exhausted the other continues alone).  Calls f(t, k) for
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int e = 0; e < 16; ++e) {
           const float2 x = fma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sl2, nm);
           float2 pp;
-          if ((kEmuMask2 >> (e & 7)) & 1) {
+          if (((D == 64 ? kEmuMask2_64 : kEmuMask2_128) >> (e & 7)) & 1) {
             pp = ex2_poly2(x);
           } else {
             pp.x = ex2(x.x);
