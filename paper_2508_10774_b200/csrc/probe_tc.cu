@@ -4,15 +4,18 @@
 //
 // CTA = 128 sampled query rows (M = 128) of one unit, streaming every
 // 128-key tile of that unit's sampled keys K_s:
-//   warps 0-7  row statistics; two warpgroups split each 128-key tile into
-//              column halves, thread = sampled query row = TMEM lane:
+//   warps 0..4H-1  row statistics; H warpgroups split each 128-key tile
+//              into 128/H-column groups, thread = sampled query row = TMEM lane:
 //              running max M and sum l of e^{s - M} over all sampled keys
 //              (l.12-15), and the per-(row, key-block) max R (l.15) kept in
 //              TMEM beside the S buffers; at the end
 //              P_imp[i, j] = max over the k rows of block i of e^{R - M} / l
 //              (l.17-19) with a 16/32-lane shuffle max.
-//   warp  8    tcgen05.mma issuer (S = Q_s K_s^T, double-buffered in TMEM)
-//   warp  9    TMA producer (Q_s tile once, K_s tiles through a smem ring)
+//   warp  4H   tcgen05.mma issuer (S = Q_s K_s^T, double-buffered in TMEM)
+//   warp  4H+1 TMA producer (Q_s tile once, K_s tiles through a smem ring)
+// H = 4 (16 softmax warps, four per SM sub-partition): the per-tile chain
+// (TMEM load, block maxima, exponentials, tree sum) is latency-bound, and
+// twice the warps of H = 2 hide twice the latency.
 // TMEM: S0 [0,128) S1 [128,256) R [256, 256 + N_b)  (N_b <= 256).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -38,16 +41,22 @@ struct PCfg {
   static constexpr int kOffBar = kOffRing + kRing * kTile;
   static constexpr int kNumBar = 1 + 2 * kRing + 4;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
-  static constexpr int kSmem = kOffMisc + 16 + 8 * 16 * 4 + 2 * 128 * 4 + 2 * 128 * 8 + 1024;
+  static constexpr int kSmem = kOffMisc + 16 + 8 * 16 * 4 + 4 * 128 * 4 + 4 * 128 * 8 + 1024;
 };
 
-constexpr int kPThreads = 384;
+#ifndef BLADE_PROBE_GROUPS
+#define BLADE_PROBE_GROUPS 4
+#endif
+constexpr int kH = BLADE_PROBE_GROUPS;      // column groups (softmax warpgroups)
+constexpr int kEW = 4 * kH;                 // softmax warps
+constexpr int kWarpMma = kEW, kWarpTma = kEW + 1;
+constexpr int kPThreads = 32 * (kEW + 2);
 // Selecting in the probe's epilogue runs select.cuh's large unrolled sort once
 // per warp per CTA from a cold instruction cache, after the CTA's tensor work;
 // the separate select kernel (mask_kernels.cu) keeps it warm across rows.
 #ifndef BLADE_PROBE_FUSED_SELECT
 #define BLADE_PROBE_FUSED_SELECT 0
-#endif  // warps 0-7 softmax, 8 MMA, 9 TMA, 10-11 idle
+#endif
 
 template <int D, int KK>
 __global__ void __launch_bounds__(kPThreads, 1)
@@ -77,7 +86,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int k_last = min(KK, N - (Nb - 1) * b);
   const int first_invalid = (Nb - 1) * KK + k_last;  // sampled columns >= this are padding
 
-  if (warp == 9 && lane == 0) {
+  if (warp == kWarpTma && lane == 0) {
     tc::mbar_init(bar_q, 1);
     for (int s = 0; s < C::kRing; ++s) {
       tc::mbar_init(bar_full + s, 1);
@@ -85,17 +94,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       tc::mbar_init(bar_s + t, 1);
-      tc::mbar_init(bar_f + t, 8);
+      tc::mbar_init(bar_f + t, kEW);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 8) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == kWarpMma) tc::tmem_alloc<512>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 9) {
+  if (warp == kWarpTma) {
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmQs);
       tc::tma_prefetch_desc(&tmKs);
@@ -111,7 +120,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                           t * 128, int(u));
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == kWarpMma) {
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       const uint32_t qa = smem_u32(sQ), rb = smem_u32(sRing);
@@ -133,13 +142,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tc::commit(bar_empty + s);
       }
     }
-  } else if (warp < 8) {
-    // two warpgroups split each 128-key tile: half h owns columns [64h, 64h+64)
-    // (key blocks [h*G/2, (h+1)*G/2) of the tile) with its own running (M, l)
-    constexpr int GH = G / 2;
+  } else if (warp < kEW) {
+    // kH warpgroups split each 128-key tile: group h owns columns [CW h, CW (h+1))
+    // (key blocks [h*GH, (h+1)*GH) of the tile) with its own running (M, l)
+    constexpr int CW = 128 / kH;
+    constexpr int GH = G / kH;
+    static_assert(GH >= 1, "a column group must hold whole key blocks");
     const int h = warp >> 2, quad = warp & 3;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    // l is kept in fp64 across tiles and each tile's 64 terms are summed as a
+    // l is kept in fp64 across tiles and each tile's CW terms are summed as a
     // tree: the sequential fp32 sum over N_k terms would dominate the probe's
     // error budget (DESIGN.md §Tie band)
     float m_run = -INFINITY;
@@ -148,26 +159,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int bsel = t & 1;
       tc::mbar_wait(bar_s + bsel, (t >> 1) & 1);
       tc::fence_after_sync();
-      float s[64];
+      float s[CW];
       {
-        uint32_t r0[32], r1[32];
-        const uint32_t ta = tmem + lane_base + bsel * 128 + h * 64;
-        tc::ld_32x32b_x32(ta + 0, r0);
-        tc::ld_32x32b_x32(ta + 32, r1);
-        tc::wait_ld();
+        const uint32_t ta = tmem + lane_base + bsel * 128 + h * CW;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          s[e] = __uint_as_float(r0[e]);
-          s[32 + e] = __uint_as_float(r1[e]);
+        for (int q = 0; q < CW / 32; ++q) {
+          uint32_t r0[32];
+          tc::ld_32x32b_x32(ta + q * 32, r0);
+          tc::wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[q * 32 + e] = __uint_as_float(r0[e]);
         }
       }
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bar_f + bsel);  // S buffer may be overwritten now
-      const int col0 = t * 128 + h * 64;
-      if (col0 + 64 > first_invalid) {
+      const int col0 = t * 128 + h * CW;
+      if (col0 + CW > first_invalid) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
+        for (int c = 0; c < CW; ++c)
           if (col0 + c >= first_invalid) s[c] = -INFINITY;
       }
       // R: per key-block max of the raw logits (Alg. 3 l.12/l.15); M and R stay
@@ -185,8 +195,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint32_t rcol = tmem + lane_base + 256 + t * G + h * GH;
       if constexpr (GH == 4) {
         tc::st_32x32b_x4(rcol, reinterpret_cast<uint32_t(&)[4]>(rv));
-      } else {
+      } else if constexpr (GH == 2) {
         tc::st_32x32b_x2(rcol, reinterpret_cast<uint32_t(&)[2]>(rv));
+      } else {
+        tc::st_32x32b_x1(rcol, reinterpret_cast<uint32_t(&)[1]>(rv));
       }
       // online row max / sum over this half (l.13-15)
       const float m_new = fmaxf(m_run, tmax);
@@ -195,13 +207,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // (s - M) * scale and tree sum, half the FMA-pipe issue slots
         const float2 nm2 = make_float2(-m_new, -m_new), sc2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
+        for (int c = 0; c < CW; c += 2) {
           const float2 x = mul2(add2(make_float2(s[c], s[c + 1]), nm2), sc2);
           s[c] = ex2(x.x);
           s[c + 1] = ex2(x.y);
         }
 #pragma unroll
-        for (int w = 32; w >= 2; w >>= 1)
+        for (int w = CW / 2; w >= 2; w >>= 1)
 #pragma unroll
           for (int c = 0; c < w; c += 2) {
             const float2 y = add2(make_float2(s[c], s[c + 1]), make_float2(s[c + w], s[c + w + 1]));
@@ -215,24 +227,29 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     }
     tc::wait_st();
-    // merge the two halves' (M, l) per row (the l.14 recurrence, once)
-    float* smm = reinterpret_cast<float*>(keep_bits + 8 * 16);        // [2][128] m
-    double* sml = reinterpret_cast<double*>(smm + 256);                 // [2][128] l
+    // merge the groups' (M, l) per row (the l.14 recurrence, once)
+    float* smm = reinterpret_cast<float*>(keep_bits + 8 * 16);        // [kH][128] m
+    double* sml = reinterpret_cast<double*>(smm + 4 * 128);             // [kH][128] l
     const int r = quad * 32 + lane;
     smm[h * 128 + r] = m_run;
     sml[h * 128 + r] = l_run;
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");
-    const float m0 = smm[r], m1 = smm[128 + r];
-    const float M = fmaxf(m0, m1);
-    const double L = (m0 == -INFINITY ? 0.0 : sml[r] * double(ex2((m0 - M) * scale_log2))) +
-                     (m1 == -INFINITY ? 0.0 : sml[128 + r] * double(ex2((m1 - M) * scale_log2)));
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kEW * 32) : "memory");
+    float M = -INFINITY;
+#pragma unroll
+    for (int g = 0; g < kH; ++g) M = fmaxf(M, smm[g * 128 + r]);
+    double L = 0.0;
+#pragma unroll
+    for (int g = 0; g < kH; ++g) {
+      const float mg = smm[g * 128 + r];
+      if (mg != -INFINITY) L += sml[g * 128 + r] * double(ex2((mg - M) * scale_log2));
+    }
     // pooling (l.17-19): rows of query block i are KK consecutive lanes; the
-    // two halves take alternate 32-column chunks of R
+    // groups take interleaved 32-column chunks of R
     const int gr = row0 + r;
     const int ib = gr / KK;
     const bool row_ok = gr < NK && (gr % KK) < min(KK, N - ib * b);
     const float inv_l = float(1.0 / L);
-    for (int j0 = h * 32; j0 < Nb; j0 += 64) {
+    for (int j0 = h * 32; j0 < Nb; j0 += 32 * kH) {
       uint32_t rr[32];
       tc::ld_32x32b_x32(tmem + lane_base + 256 + j0, rr);
       tc::wait_ld();
@@ -278,7 +295,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     }
   }
-  if (warp == 8) {
+  if (warp == kWarpMma) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
   }

@@ -169,6 +169,10 @@ BLADE_DEVINL void st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
                "r"(r[7])
                : "memory");
 }
+BLADE_DEVINL void st_32x32b_x1(uint32_t taddr, const uint32_t (&r)[1]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(taddr), "r"(r[0])
+               : "memory");
+}
 BLADE_DEVINL void st_32x32b_x2(uint32_t taddr, const uint32_t (&r)[2]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};\n" ::"r"(taddr), "r"(r[0]),
                "r"(r[1])
