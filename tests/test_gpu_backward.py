@@ -141,3 +141,32 @@ def test_gt_backward_smooth_end_to_end(A):
                                                 m.kv_cnt.cpu().numpy(), 128, 128)
     for got, ref, nm in ((dq, rq, "dq"), (dk, rk, "dk"), (dv, rv, "dv")):
         _check(got, ref, nm)
+
+
+@pytest.mark.parametrize("variant", ["asa", "asa_gt"])
+def test_backward_fullsize_wan_unit(A, variant):
+    """BASELINE.json configs[1] (Wan2.1-1.3B layer, 12 x 32760 x 128), keep
+    51/256 as bench.py times it, the bench's launch configuration (all 12
+    units in one call); the oracle recomputes unit 0's dQ, dK, dV in full
+    (every row of the unit, 256 query blocks x 6528 kept keys)."""
+    q, k, v = inputs.make("wan", "smooth")
+    do = inputs.iid(1, q.shape[0], q.shape[1], q.shape[2], seed=11)[0]
+    qd, kd, vd, dod = PT.to_dev(q, k, v, do)
+    if variant == "asa":
+        o, lse, m = A.asa_forward(qd, kd, vd, tau=0.9, keep_min=51, keep_max=51)
+        dq, dk, dv = A.blade_bsa_bwd(qd, kd, vd, o, lse, dod, m.kv_idx, m.kv_cnt)
+    else:
+        o, lse, m = A.asa_gt_forward(qd, kd, vd, window=128, tau=0.9, keep_min=51, keep_max=51)
+        kg, vg = A.blade_gt_pool(kd, vd, window=128)
+        dq, dk, dv = A.blade_bsa_gt_bwd(qd, kd, vd, kg, vg, o, lse, dod, m.kv_idx, m.kv_cnt)
+    torch.cuda.synchronize()
+    kv_idx, kv_cnt = m.kv_idx.cpu().numpy(), m.kv_cnt.cpu().numpy()
+    scale = O.default_scale(q.shape[2])
+    if variant == "asa":
+        refs = O.sparse_attention_backward_unit(q[0], k[0], v[0], do[0], kv_idx[0], kv_cnt[0],
+                                                128, scale)
+    else:
+        refs = O.sparse_attention_gt_backward_unit(q[0], k[0], v[0], do[0], kv_idx[0],
+                                                   kv_cnt[0], 128, scale, 128)
+    for got, ref, nm in zip((dq, dk, dv), refs, ("dq", "dk", "dv")):
+        _check(got[0], ref, nm)
