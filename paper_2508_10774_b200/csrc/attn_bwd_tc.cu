@@ -48,7 +48,17 @@ struct BCfg {
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
 };
 
-constexpr int kBThreads = 224;
+// EWG elementwise warpgroups split each 128-column tile into 128/EWG-column
+// groups (thread = row = TMEM lane, as before).  EWG = 2 for d = 64, where the
+// elementwise work (exponentials, dS) outweighs the tensor work per item; P /
+// dS then go to TMEM columns of their own (no group overwrites columns another
+// group has not read yet): dQ kernel [384, 448), dK/dV kernel [384, 512).
+// Warps: 0..4 EWG-1 elementwise, 4 EWG MMA, 4 EWG + 1 / + 2 TMA.
+template <int EWG>
+constexpr int bwd_threads() { return 32 * (4 * EWG + 3); }
+#ifndef BLADE_BWD_EWG64
+#define BLADE_BWD_EWG64 2
+#endif
 
 // ASA_GT (attn_bwd.cu header): the global tokens as extra 128-row items.
 struct BwdGtArgs {
@@ -64,8 +74,8 @@ BLADE_DEVINL float gt_bias2(const BwdGtArgs& g, int w) {
   return w < g.Ng - 1 ? g.bfull2 : (w == g.Ng - 1 ? g.blast2 : -INFINITY);
 }
 
-template <int D, bool kGT>
-__global__ void __launch_bounds__(kBThreads, 1)
+template <int D, bool kGT, int EWG>
+__global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmKg,
@@ -94,13 +104,16 @@ __global__ void __launch_bounds__(kBThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kEW = 4 * EWG, kWMma = kEW, kWTmaK = kEW + 1, kWTmaV = kEW + 2;
+  constexpr int CW = 128 / EWG;                               // columns per group
+  constexpr uint32_t kColDS = EWG == 1 ? C::kColDP : 384;     // packed bf16 dS
   const int i = blockIdx.x;
   const int64_t u = blockIdx.y;
   const int cnt = kv_cnt[u * Nb + i];
   const int32_t* list = kv_idx + (u * Nb + i) * Nb;
   const int total = cnt + (kGT ? gt.ngt : 0);  // kept blocks, then global-token tiles
 
-  if (warp == 5 && lane == 0) {
+  if (warp == kWTmaK && lane == 0) {
     tc::mbar_init(bar_q, 1);
     for (int s = 0; s < C::kRingK; ++s) {
       tc::mbar_init(bar_kfull + s, 1);
@@ -112,21 +125,21 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
     tc::mbar_init(bar_sc, 1);
     tc::mbar_init(bar_dp, 1);
-    tc::mbar_init(bar_sf, 4);
-    tc::mbar_init(bar_ds, 4);
+    tc::mbar_init(bar_sf, kEW);
+    tc::mbar_init(bar_ds, kEW);
     tc::mbar_init(bar_dq, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 4) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == kWMma) tc::tmem_alloc<512>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5 || warp == 6) {
+  if (warp == kWTmaK || warp == kWTmaV) {
     // ===================== TMA producers =====================
     if (lane == 0) {
-      const bool isK = warp == 5;
+      const bool isK = warp == kWTmaK;
       if (isK) {
         tc::tma_prefetch_desc(&tmQ);
         tc::tma_prefetch_desc(&tmDO);
@@ -156,7 +169,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
                           int(u));
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kWMma) {
     // ===================== MMA issuer =====================
     if (lane == 0 && total > 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
@@ -200,7 +213,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
         const uint32_t kb = kbase + (n % C::kRingK) * C::kTile;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          tc::mma_ts(tmem + C::kColDQ, tmem + C::kColDP + ks * 8,
+          tc::mma_ts(tmem + C::kColDQ, tmem + kColDS + ks * 8,
                      tc::sw128_desc(kb + ks * 2048, C::kPanel, 1024), idQ,
                      (n > 0 || ks > 0) ? 1 : 0);
         tc::commit(bar_dq);
@@ -209,10 +222,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
       }
       tc::mbar_wait(bar_dq, (total - 1) & 1);
     }
-  } else if (warp < 4) {
+  } else if (warp < kEW) {
     // ===================== elementwise: P, dS =====================
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
-    const int r = warp * 32 + lane;
+    const int hg = warp / 4, quad = warp & 3;  // column group, TMEM lane quarter
+    const uint32_t lane_base = uint32_t(quad * 32) << 16;
+    const int r = quad * 32 + lane;
+    const int c0 = hg * CW;                    // first column of this group
     const int row = i * 128 + r;
     const float sl2 = scale * kLog2e;
     const float lse2 = row < N ? LSE[u * N + row] * kLog2e : INFINITY;  // P = 0 past N
@@ -223,11 +238,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
       if (n + 1 < cnt) jn = __ldg(list + n + 1);
       tc::mbar_wait(bar_sc, n & 1);
       tc::fence_after_sync();
-      float p[128];
+      float p[CW];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t rr[32];
-        tc::ld_32x32b_x32(tmem + lane_base + C::kColS + c * 32, rr);
+        tc::ld_32x32b_x32(tmem + lane_base + C::kColS + c0 + c * 32, rr);
 #pragma unroll
         for (int e = 0; e < 32; ++e) p[c * 32 + e] = __uint_as_float(rr[e]);
       }
@@ -236,25 +251,25 @@ __global__ void __launch_bounds__(kBThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bar_sf);
       if (!kGT || n < cnt) {
-        const int valid = N - jb * 128;  // keys of a partial last block
+        const int valid = N - jb * 128 - c0;  // keys of a partial last block
 #pragma unroll
-        for (int c = 0; c < 128; c += 2) {
+        for (int c = 0; c < CW; c += 2) {
           const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
                                 make_float2(-lse2, -lse2));
           p[c] = c < valid ? ex2(x.x) : 0.f;
           p[c + 1] = c + 1 < valid ? ex2(x.y) : 0.f;
         }
       } else {  // global tokens w0 + c: + ln n_w
-        const int w0 = (n - cnt) * 128;
+        const int w0 = (n - cnt) * 128 + c0;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) p[c] = ex2(fmaf(p[c], sl2, gt_bias2(gt, w0 + c) - lse2));
+        for (int c = 0; c < CW; ++c) p[c] = ex2(fmaf(p[c], sl2, gt_bias2(gt, w0 + c) - lse2));
       }
       tc::mbar_wait(bar_dp, n & 1);
       tc::fence_after_sync();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t rr[32];
-        tc::ld_32x32b_x32(tmem + lane_base + C::kColDP + c * 32, rr);
+        tc::ld_32x32b_x32(tmem + lane_base + C::kColDP + c0 + c * 32, rr);
         tc::wait_ld();
         uint32_t pk[16];
 #pragma unroll
@@ -265,7 +280,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
         }
         // dS of keys [32c, 32c+32) -> packed columns [16c, 16c+16) of the dP
         // region: columns this thread has already read
-        tc::st_32x32b_x16(tmem + lane_base + C::kColDP + c * 16, pk);
+        tc::st_32x32b_x16(tmem + lane_base + kColDS + c0 / 2 + c * 16, pk);
       }
       tc::wait_st();
       tc::fence_before_sync();
@@ -279,11 +294,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
     __nv_bfloat16* out = dQ + (u * N + row) * int64_t(D);
     if (total == 0) {  // no kept block (never produced by blade_asa_mask): dQ = 0
-      if (row < N)
+      if (row < N && hg == 0)
         for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
     } else
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = hg; c < D / 32; c += EWG) {
       uint32_t rr[32];
       tc::ld_32x32b_x32(tmem + lane_base + C::kColDQ + c * 32, rr);
       tc::wait_ld();
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kWMma) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
   }
@@ -341,8 +356,8 @@ struct KCfg {
 // K_g/V_g), every query block attends it, blockIdx.z splits the query blocks
 // (gt.qps each) and the sums go to fp32 partials gt.part (attn_bwd.cu reduces
 // them and spreads dK_g/n_w, dV_g/n_w over the windows).
-template <int D, bool kGT>
-__global__ void __launch_bounds__(kBThreads, 1)
+template <int D, bool kGT, int EWG>
+__global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                        const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        const BwdGtArgs gt, int N, int Nb, float scale, const float* __restrict__ LSE,
@@ -368,6 +383,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
   float* sLD = reinterpret_cast<float*>(smem + C::kOffLD);  // [buf][0: lse2, 1: D][128]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kEW = 4 * EWG, kWMma = kEW, kWTma = kEW + 1;
+  constexpr int CW = 128 / EWG;
+  static_assert(EWG == 1 || 256 + 2 * D <= 384, "separate P / dS columns need d = 64");
+  constexpr uint32_t kColP = EWG == 1 ? C::kColS : 384;      // packed bf16 P^T
+  constexpr uint32_t kColDSt = EWG == 1 ? C::kColDP : 448;   // packed bf16 dS^T
   const int j = blockIdx.x;
   const int64_t u = blockIdx.y;
   const int i_first = kGT ? int(blockIdx.z) * gt.qps : 0;
@@ -375,7 +395,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int32_t* list = kGT ? nullptr : q_idx + (u * Nb + j) * Nb;
   auto qblock = [&](int n) { return kGT ? i_first + n : __ldg(list + n); };
 
-  if (warp == 5 && lane == 0) {
+  if (warp == kWTma && lane == 0) {
     tc::mbar_init(bar_kv, 1);
     for (int s = 0; s < C::kRing; ++s) {
       tc::mbar_init(bar_full + s, 1);
@@ -383,18 +403,18 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
     tc::mbar_init(bar_sc, 1);
     tc::mbar_init(bar_dp, 1);
-    tc::mbar_init(bar_p, 4);
-    tc::mbar_init(bar_ds, 4);
+    tc::mbar_init(bar_p, kEW);
+    tc::mbar_init(bar_ds, kEW);
     tc::mbar_init(bar_dk, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 4) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == kWMma) tc::tmem_alloc<512>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5) {
+  if (warp == kWTma) {
     // ===================== TMA producer: K_j, V_j once; (Q_i, dO_i) ring =====
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmQ);
@@ -419,7 +439,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
         }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kWMma) {
     // ===================== MMA issuer =====================
     if (lane == 0 && cnt > 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
@@ -454,7 +474,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       for (int n = 0; n < cnt; ++n) {
         tc::mbar_wait(bar_p, n & 1);
         tc::fence_after_sync();
-        ts(C::kColDV, C::kColS, slot_q(n) + C::kTile, n > 0);  // dV += P^T dO_i
+        ts(C::kColDV, kColP, slot_q(n) + C::kTile, n > 0);  // dV += P^T dO_i
         if (n + 1 < cnt) {
           wait_full(n + 1);
           ss(C::kColS, ka, slot_q(n + 1));         // S^T(n+1) (after dV(n) read P^T(n))
@@ -462,7 +482,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
         }
         tc::mbar_wait(bar_ds, n & 1);
         tc::fence_after_sync();
-        ts(C::kColDK, C::kColDP, slot_q(n), n > 0);  // dK += dS^T Q_i
+        ts(C::kColDK, kColDSt, slot_q(n), n > 0);  // dK += dS^T Q_i
         tc::commit(bar_dk);
         tc::commit(bar_empty + (n % C::kRing));
         if (n + 1 < cnt) {
@@ -472,10 +492,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
       }
       tc::mbar_wait(bar_dk, (cnt - 1) & 1);
     }
-  } else if (warp < 4) {
+  } else if (warp < kEW) {
     // ===================== elementwise: P^T, dS^T (thread = key row) ========
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
-    const int r = warp * 32 + lane;
+    const int hg = warp / 4, quad = warp & 3;
+    const uint32_t lane_base = uint32_t(quad * 32) << 16;
+    const int r = quad * 32 + lane;
+    const int c0 = hg * CW;
     const float sl2 = scale * kLog2e;
     const float brow = kGT ? gt_bias2(gt, j * 128 + r) : 0.f;  // ln n_w of this key row
     int in = cnt > 0 ? qblock(0) : 0;
@@ -483,37 +505,38 @@ __global__ void __launch_bounds__(kBThreads, 1)
       const int ib = in;
       if (n + 1 < cnt) in = qblock(n + 1);
       float* L = sLD + (n & 1) * 256;
-      {  // stage LSE_i (log2 domain) and D_i: query column r
+      if (hg == 0) {  // stage LSE_i (log2 domain) and D_i: query column r
         const int qrow = ib * 128 + r;
         L[r] = qrow < N ? LSE[u * N + qrow] * kLog2e : INFINITY;  // P = 0 past N
         L[128 + r] = qrow < N ? Dv[u * N + qrow] : 0.f;
       }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kEW * 32) : "memory");
       tc::mbar_wait(bar_sc, n & 1);
       tc::fence_after_sync();
-      float p[128];
+      float p[CW];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t rr[32];
-        tc::ld_32x32b_x32(tmem + lane_base + C::kColS + c * 32, rr);
+        tc::ld_32x32b_x32(tmem + lane_base + C::kColS + c0 + c * 32, rr);
 #pragma unroll
         for (int e = 0; e < 32; ++e) p[c * 32 + e] = __uint_as_float(rr[e]);
       }
       tc::wait_ld();
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
+      for (int c = 0; c < CW; c += 2) {
+        const float* Lc = L + c0;
         const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
-                              kGT ? make_float2(brow - L[c], brow - L[c + 1])
-                                  : make_float2(-L[c], -L[c + 1]));
+                              kGT ? make_float2(brow - Lc[c], brow - Lc[c + 1])
+                                  : make_float2(-Lc[c], -Lc[c + 1]));
         p[c] = ex2(x.x);
         p[c + 1] = ex2(x.y);
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // P^T (bf16) -> packed columns [16c, 16c+16) of S^T
+      for (int c = 0; c < CW / 32; ++c) {  // P^T (bf16) -> packed columns
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(p[c * 32 + 2 * e], p[c * 32 + 2 * e + 1]);
-        tc::st_32x32b_x16(tmem + lane_base + C::kColS + c * 16, pk);
+        tc::st_32x32b_x16(tmem + lane_base + kColP + c0 / 2 + c * 16, pk);
       }
       tc::wait_st();
       tc::fence_before_sync();
@@ -522,19 +545,19 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tc::mbar_wait(bar_dp, n & 1);
       tc::fence_after_sync();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t rr[32];
-        tc::ld_32x32b_x32(tmem + lane_base + C::kColDP + c * 32, rr);
+        tc::ld_32x32b_x32(tmem + lane_base + C::kColDP + c0 + c * 32, rr);
         tc::wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int q0 = c * 32 + 2 * e;
-          const float d0 = p[q0] * (__uint_as_float(rr[2 * e]) - L[128 + q0]);
-          const float d1 = p[q0 + 1] * (__uint_as_float(rr[2 * e + 1]) - L[128 + q0 + 1]);
+          const float d0 = p[q0] * (__uint_as_float(rr[2 * e]) - L[128 + c0 + q0]);
+          const float d1 = p[q0 + 1] * (__uint_as_float(rr[2 * e + 1]) - L[128 + c0 + q0 + 1]);
           pk[e] = pack_bf16(d0, d1);
         }
-        tc::st_32x32b_x16(tmem + lane_base + C::kColDP + c * 16, pk);  // already-read columns
+        tc::st_32x32b_x16(tmem + lane_base + kColDSt + c0 / 2 + c * 16, pk);
       }
       tc::wait_st();
       tc::fence_before_sync();
@@ -550,7 +573,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     if constexpr (kGT) {  // fp32 partials (dK_g scaled), every row of the tile
       const int Ngp = gt.ngt * 128;
 #pragma unroll
-      for (int which = 0; which < 2; ++which) {
+      for (int which = EWG == 2 ? hg : 0; which < 2; which += EWG) {
         float* out = gt.part + which * gt.part_stride +
                      ((int64_t(blockIdx.z) * gridDim.y + u) * Ngp + krow) * int64_t(D);
         const float z = which ? 1.f : scale;
@@ -573,7 +596,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       }
     } else
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
+    for (int which = EWG == 2 ? hg : 0; which < 2; which += EWG) {
       __nv_bfloat16* out = (which ? dV : dK) + (u * N + krow) * int64_t(D);
       const float z = which ? 1.f : scale;
       if (cnt == 0) {
@@ -602,7 +625,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kWMma) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
   }
@@ -630,11 +653,12 @@ cudaError_t launch_dkdv_d(const AttnProblem& p, const void* q, const void* k, co
     ga.part = part;
     ga.part_stride = int64_t(splits) * p.BH * ga.ngt * 128 * D;
   }
-  auto kern = g ? bwd_dkdv_tc_kernel<D, true> : bwd_dkdv_tc_kernel<D, false>;
+  constexpr int EWG = D == 64 ? BLADE_BWD_EWG64 : 1;
+  auto kern = g ? bwd_dkdv_tc_kernel<D, true, EWG> : bwd_dkdv_tc_kernel<D, false, EWG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(g ? ga.ngt : p.Nb), unsigned(p.BH), unsigned(g ? splits : 1));
-  kern<<<grid, kBThreads, smem, stream>>>(
+  kern<<<grid, bwd_threads<EWG>(), smem, stream>>>(
       mq, mdo, mk, mv, ga, p.N, p.Nb, p.scale, lse, Dv, q_idx, q_cnt,
       reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
   return cudaGetLastError();
@@ -662,11 +686,12 @@ cudaError_t launch_dq_d(const AttnProblem& p, const void* q, const void* k, cons
     mvg = mv;
   }
   constexpr int smem = BCfg<D>::kSmem;
-  auto kern = g ? bwd_dq_tc_kernel<D, true> : bwd_dq_tc_kernel<D, false>;
+  constexpr int EWG = D == 64 ? BLADE_BWD_EWG64 : 1;
+  auto kern = g ? bwd_dq_tc_kernel<D, true, EWG> : bwd_dq_tc_kernel<D, false, EWG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(p.Nb), unsigned(p.BH));
-  kern<<<grid, kBThreads, smem, stream>>>(mq, mdo, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale, lse,
+  kern<<<grid, bwd_threads<EWG>(), smem, stream>>>(mq, mdo, mk, mv, mkg, mvg, ga, p.N, p.Nb, p.scale, lse,
                                           Dv, kv_idx, kv_cnt,
                                           reinterpret_cast<__nv_bfloat16*>(dq));
   return cudaGetLastError();
