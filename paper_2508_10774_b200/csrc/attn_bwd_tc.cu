@@ -22,6 +22,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "attn_common.cuh"
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
@@ -57,8 +58,17 @@ struct BCfg {
 template <int EWG>
 constexpr int bwd_threads() { return 32 * (4 * EWG + 3); }
 #ifndef BLADE_BWD_EWG64
-#define BLADE_BWD_EWG64 2
+#define BLADE_BWD_EWG64 2  // A/B on Cog: 3.28 ms (2) vs 3.54 (1) vs 3.38 (4)
 #endif
+// Which of every 8 exponential pairs of P run on the FMA pipe
+// (attn::ex2_poly2, rel. error < 7.5e-5, below the bf16 rounding of P).
+#ifndef BLADE_BWD_EMU_MASK
+#define BLADE_BWD_EMU_MASK 0x01  // 1 in 8: Cog 3.280 ms vs 3.315 (1 in 4), 3.332 (none), 3.43 (1 in 2)
+#endif
+BLADE_DEVINL float2 bwd_ex2_pair(float2 x, int pair) {
+  if ((BLADE_BWD_EMU_MASK >> (pair & 7)) & 1) return attn::ex2_poly2(x);
+  return make_float2(ex2(x.x), ex2(x.y));
+}
 
 // ASA_GT (attn_bwd.cu header): the global tokens as extra 128-row items.
 struct BwdGtArgs {
@@ -254,10 +264,10 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
         const int valid = N - jb * 128 - c0;  // keys of a partial last block
 #pragma unroll
         for (int c = 0; c < CW; c += 2) {
-          const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
-                                make_float2(-lse2, -lse2));
-          p[c] = c < valid ? ex2(x.x) : 0.f;
-          p[c + 1] = c + 1 < valid ? ex2(x.y) : 0.f;
+          const float2 x = bwd_ex2_pair(fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
+                                             make_float2(-lse2, -lse2)), c / 2);
+          p[c] = c < valid ? x.x : 0.f;
+          p[c + 1] = c + 1 < valid ? x.y : 0.f;
         }
       } else {  // global tokens w0 + c: + ln n_w
         const int w0 = (n - cnt) * 128 + c0;
@@ -525,11 +535,12 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
 #pragma unroll
       for (int c = 0; c < CW; c += 2) {
         const float* Lc = L + c0;
-        const float2 x = fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
-                              kGT ? make_float2(brow - Lc[c], brow - Lc[c + 1])
-                                  : make_float2(-Lc[c], -Lc[c + 1]));
-        p[c] = ex2(x.x);
-        p[c + 1] = ex2(x.y);
+        const float2 x = bwd_ex2_pair(
+            fma2(make_float2(p[c], p[c + 1]), make_float2(sl2, sl2),
+                 kGT ? make_float2(brow - Lc[c], brow - Lc[c + 1]) : make_float2(-Lc[c], -Lc[c + 1])),
+            c / 2);
+        p[c] = x.x;
+        p[c + 1] = x.y;
       }
 #pragma unroll
       for (int c = 0; c < CW / 32; ++c) {  // P^T (bf16) -> packed columns
@@ -573,7 +584,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     if constexpr (kGT) {  // fp32 partials (dK_g scaled), every row of the tile
       const int Ngp = gt.ngt * 128;
 #pragma unroll
-      for (int which = EWG == 2 ? hg : 0; which < 2; which += EWG) {
+      for (int which = hg; which < 2; which += EWG) {
         float* out = gt.part + which * gt.part_stride +
                      ((int64_t(blockIdx.z) * gridDim.y + u) * Ngp + krow) * int64_t(D);
         const float z = which ? 1.f : scale;
@@ -596,7 +607,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
       }
     } else
 #pragma unroll
-    for (int which = EWG == 2 ? hg : 0; which < 2; which += EWG) {
+    for (int which = hg; which < 2; which += EWG) {
       __nv_bfloat16* out = (which ? dV : dK) + (u * N + krow) * int64_t(D);
       const float z = which ? 1.f : scale;
       if (cnt == 0) {
