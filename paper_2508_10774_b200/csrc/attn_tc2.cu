@@ -61,7 +61,7 @@ struct Cfg2 {
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
   static constexpr int kOffBar = kOffRingV + kRingV * kTile;
   // bar_q, kfull/kempty, vfull/vempty, per block: s, p, pv
-  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 4 * 2;
+  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 6 * 2;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
   static constexpr int kSmem = kOffMisc + 16 + 1024;  // + alignment slack
   static constexpr uint32_t kColO = 256;
@@ -74,6 +74,22 @@ struct Cfg2 {
 #endif
   static constexpr bool kSepP = D == 64 && BLADE_ATTN2_SEP_P;
   static constexpr uint32_t kColP = 256 + 2 * D;
+  // Half-tile S pipeline: S = Q K^T as two N = 64 MMAs (keys [0, 64) "early",
+  // [64, 128) "late") into the two 64-column halves of the block's S region,
+  // which alternate roles tile by tile: E_k (early S of tile k, then P(k))
+  // and L_k (late S of tile k).  S_early(k+1) goes to L_k as soon as the
+  // softmax has read S_late(k), so the softmax of tile k+1 starts on its first
+  // half while the tensor core runs P V(k) and S_late(k+1) (into E_k, after
+  // P V(k) has read P(k)).  The online max is lazy (threshold 2^8) per half;
+  // a late-half rescale also rescales the already stored early-half P.
+  // Parity green but slower (Wan 1.39-1.41 vs 1.155 ms, Cog 1.17 vs 1.04 ms,
+  // interleaved A/B): two N = 64 S MMAs read Q twice, 96 instead of 64 KB of
+  // shared memory per tile for S, and the d = 128 kernel is bound by shared-
+  // memory bandwidth, so off by default.
+#ifndef BLADE_ATTN2_HALF_S
+#define BLADE_ATTN2_HALF_S 0
+#endif
+  static constexpr bool kHalfS = BLADE_ATTN2_HALF_S && !kSepP;
 };
 
 constexpr int kThreads2 = 384;
@@ -138,6 +154,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint64_t* bar_p = bar_s + 2;               // [2] P of block t written (4 warp arrivals)
   uint64_t* bar_pv = bar_p + 2;              // [2] P V of block t done
   uint64_t* bar_sf = bar_pv + 2;             // [2] S of block t read out (kSepP, 4 warps)
+  uint64_t* bar_sl = bar_sf + 2;             // [2] late half of S computed (kHalfS)
+  uint64_t* bar_slf = bar_sl + 2;            // [2] late half of S read out (kHalfS, 4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -174,6 +192,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::mbar_init(bar_p + t, 4);
       tc::mbar_init(bar_pv + t, 1);
       tc::mbar_init(bar_sf + t, 4);
+      tc::mbar_init(bar_sl + t, 1);
+      tc::mbar_init(bar_slf + t, 4);
     }
     tc::fence_barrier_init();
   }
@@ -281,6 +301,64 @@ __global__ void __launch_bounds__(kThreads2, 1)
         tc::commit(bar_vempty + s);
         ++gv;
       };
+      if constexpr (C::kHalfS) {
+        constexpr uint32_t idS64 = tc::idesc_bf16(128, 64, 0, 0);
+        int kslot[2] = {0, 0};
+        // half h of S_t(k) (keys [64h, 64h+64)) into column half `dst` of S_t
+        auto issue_Sh = [&](int t, int k, int h) {
+          if (h == 0) {  // first use of item (t, k)'s K slot
+            const int s = gk % C::kRingK;
+            tc::mbar_wait(bar_kfull + s, (gk / C::kRingK) & 1);
+            tc::fence_after_sync();
+            kslot[t] = s;
+            ++gk;
+          }
+          const int s = kslot[t];
+          const uint32_t kb = kbase + s * C::kTile + h * 8192, qb = qbase + t * C::kTile;
+          const uint32_t dst = t * 128 + ((k & 1) ^ h) * 64;  // early: E_k, late: L_k
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
+            tc::mma_ss(tmem + dst, tc::sw128_desc(qb + off, 16, 1024),
+                       tc::sw128_desc(kb + off, 16, 1024), idS64, ks > 0);
+          }
+          tc::commit(h ? bar_sl + t : bar_s + t);
+          if (h) tc::commit(bar_kempty + s);
+        };
+        auto issue_PVh = [&](int t, int k) {  // O_t += P_t(k) V, P_t(k) in E_k
+          const int s = gv % C::kRingV;
+          tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
+          tc::mbar_wait(bar_p + t, k & 1);
+          tc::fence_after_sync();
+          const uint32_t vb = vbase + s * C::kTile;
+          const uint32_t pcol = t * 128 + (k & 1) * 64;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
+                       tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
+                       (k > 0 || ks > 0) ? 1 : 0);
+          tc::commit(bar_pv + t);
+          tc::commit(bar_vempty + s);
+          ++gv;
+        };
+        for (int t = 0; t < 2; ++t)
+          if ((t ? cnt1 : cnt0) > 0) {
+            issue_Sh(t, 0, 0);
+            issue_Sh(t, 0, 1);
+          }
+        const int m = cnt0 > cnt1 ? cnt0 : cnt1;
+        for (int k = 0; k < m; ++k)
+          for (int t = 0; t < 2; ++t) {
+            const int c = t ? cnt1 : cnt0;
+            if (k >= c) continue;
+            if (k + 1 < c) {  // L_k free once the softmax has read S_late(k)
+              tc::mbar_wait(bar_slf + t, k & 1);
+              issue_Sh(t, k + 1, 0);
+            }
+            issue_PVh(t, k);
+            if (k + 1 < c) issue_Sh(t, k + 1, 1);  // into E_k, after P V(k) read P(k)
+          }
+      } else {
       if (cnt0 > 0) issue_S(0, 0);
       if (cnt1 > 0) issue_S(1, 0);
       const int m = cnt0 > cnt1 ? cnt0 : cnt1;
@@ -307,6 +385,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           }
         }
       }
+      }  // !kHalfS
       // drain: the last commits must land before the CTA's smem is released
       if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, (cnt0 - 1) & 1);
       if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, (cnt1 - 1) & 1);
@@ -325,6 +404,138 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int r = qw * 32 + lane;
     float m_used = -INFINITY, l_sum = 0.f;
     int jn = cnt_fine > 0 ? __ldg(list) : 0;  // block id, loaded one tile ahead
+    if constexpr (C::kHalfS) {
+      const float2 sl2 = make_float2(scale_log2, scale_log2);
+      // rescale O_t (and l) by f; O_t must be current
+      auto rescale_o = [&](float f) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t rr[32];
+          tc::ld_32x32b_x32(tO + c * 32, rr);
+          tc::wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * f);
+          tc::st_32x32b_x32(tO + c * 32, rr);
+        }
+      };
+      // 64 scores of half h (keys [64h, 64h+64)) from TMEM column base `col`,
+      // masked / biased; returns their max
+      auto load_half = [&](uint32_t col, int h, int n, int jb, float (&x)[64]) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t rr[32];
+          tc::ld_32x32b_x32(col + c * 32, rr);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) x[c * 32 + e] = __uint_as_float(rr[e]);
+        }
+        tc::wait_ld();
+        const bool fine = !kGT || n < cnt_fine;
+        const int valid = (fine ? N - jb * 128 : gt.Ng - (n - cnt_fine) * 128) - 64 * h;
+        if (valid < 64) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c >= valid) x[c] = -INFINITY;
+        }
+        if (kGT && !fine) {
+          const int last = gt.Ng - 1 - (n - cnt_fine) * 128 - 64 * h;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) x[c] += c == last ? gt.bias_last : gt.bias_full;
+        }
+        float t4[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float m4 = fmaxf(x[g], x[g + 4]);
+#pragma unroll
+          for (int c = g + 8; c < 64; c += 8) m4 = fmaxf(m4, fmaxf(x[c], x[c + 4]));
+          t4[g] = m4;
+        }
+        return fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+      };
+      // P = 2^(s scale - m_used) of a half -> packed bf16 columns [32h, 32h+32) of E
+      auto exp_store = [&](const float (&x)[64], uint32_t ecol, int h) {
+        float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
+        const float2 nm = make_float2(-m_used, -m_used);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 xx = fma2(make_float2(x[c * 32 + 2 * e], x[c * 32 + 2 * e + 1]), sl2, nm);
+            float2 pp;
+            if (((D == 64 ? kEmuMask2_64 : kEmuMask2_128) >> (e & 7)) & 1) {
+              pp = ex2_poly2(xx);
+            } else {
+              pp.x = ex2(xx.x);
+              pp.y = ex2(xx.y);
+            }
+            acc4[e & 3] = add2(acc4[e & 3], pp);
+            pk[e] = pack_bf16(pp.x, pp.y);
+          }
+          tc::st_32x32b_x16(ecol + 32 * h + c * 16, pk);
+        }
+        const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
+        l_sum += acc.x + acc.y;
+      };
+      for (int n = 0; n < cnt; ++n) {
+        const int jb = jn;
+        if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
+        const uint32_t E = tS + (n & 1) * 64, Lc = tS + ((n & 1) ^ 1) * 64;
+        float x[64];
+        // ---- early half (keys [0, 64)) in E_n
+        tc::mbar_wait(bar_s + t, n & 1);
+        tc::fence_after_sync();
+        {
+          const float mxs = load_half(E, 0, n, jb, x) * scale_log2;
+          if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
+            const float m_new = fmaxf(m_used, mxs);
+            if (n > 0) {  // O_t current: P V(n-1) done
+              tc::mbar_wait(bar_pv + t, (n - 1) & 1);
+              tc::fence_after_sync();
+              const float f = ex2(m_used - m_new);
+              l_sum *= f;
+              rescale_o(f);
+            }
+            m_used = m_new;
+          }
+        }
+        exp_store(x, E, 0);
+        // ---- late half (keys [64, 128)) in L_n
+        tc::mbar_wait(bar_sl + t, n & 1);
+        tc::fence_after_sync();
+        {
+          const float mxs = load_half(Lc, 1, n, jb, x) * scale_log2;
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(bar_slf + t);  // L_n may take S_early(n+1)
+          if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
+            // S_late(n) complete => P V(n-1) complete (issued before it)
+            const float m_new = fmaxf(m_used, mxs);
+            const float f = ex2(m_used - m_new);
+            l_sum *= f;
+            if (n > 0) rescale_o(f);
+            tc::wait_st();
+            {  // the early half's P, already stored with the old max
+              uint32_t rr[32];
+              tc::ld_32x32b_x32(E, rr);
+              tc::wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const float2 v = unpack_bf16(rr[e]);
+                rr[e] = pack_bf16(v.x * f, v.y * f);
+              }
+              tc::st_32x32b_x32(E, rr);
+            }
+            m_used = m_new;
+          }
+        }
+        exp_store(x, E, 1);
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar_p + t);
+      }
+    } else
     for (int n = 0; n < cnt; ++n) {
       const int jb = jn;
       if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);

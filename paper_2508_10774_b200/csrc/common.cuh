@@ -62,6 +62,10 @@ BLADE_DEVINL uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+BLADE_DEVINL float2 unpack_bf16(uint32_t v) {  // inverse of pack_bf16 (exact)
+  return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+}
+
 BLADE_DEVINL float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
