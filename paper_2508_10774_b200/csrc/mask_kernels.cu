@@ -315,8 +315,13 @@ __global__ void __launch_bounds__(128) probe_kernel(const __nv_bfloat16* __restr
 // probe selects its own rows in its epilogue).  One warp per row.
 // ---------------------------------------------------------------------------
 constexpr int SEL_WARPS = 4;
+// 6 CTAs per SM (<= 85 registers): the Wan layer's 768 CTAs fit one wave
+// (at 96 registers, 5 per SM, 1.04 waves)
+#ifndef BLADE_SEL_MIN_BLOCKS
+#define BLADE_SEL_MIN_BLOCKS 6
+#endif
 
-__global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(
+__global__ void __launch_bounds__(SEL_WARPS * 32, BLADE_SEL_MIN_BLOCKS) select_kernel(
     const float* __restrict__ pimp, int64_t rows, int Nb, double tau, int lo, int hi,
     double guard, uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx,
     int32_t* __restrict__ kv_cnt, int* __restrict__ counters, int32_t* __restrict__ flags,
