@@ -422,18 +422,25 @@ def main():
 
     # the production single call (blade_asa_fwd: the attention launched as a
     # programmatic dependent of the mask's last kernel), same inputs
+    # (ASA_GT: blade_asa_gt_fwd, MeanPool_n + mask + attention in one call)
     fused_ms = None
-    if not gt:
-        fo = A.blade_asa_fwd(q, k, v, unit_offset=unit_offset, impl=impl, **mp)
+    if not (gt and impl == A.ATTN_MMA_SYNC):
+        def fused(out=None):
+            if gt:
+                return A.blade_asa_gt_fwd(q, k, v, window=args.window, unit_offset=unit_offset,
+                                          impl=impl, out=out, **mp)
+            return A.blade_asa_fwd(q, k, v, unit_offset=unit_offset, impl=impl, out=out, **mp)
+
+        fo = fused()
         for _ in range(3):
-            A.blade_asa_fwd(q, k, v, unit_offset=unit_offset, impl=impl, out=fo, **mp)
+            fused(fo)
         if ws > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):
-            A.blade_asa_fwd(q, k, v, unit_offset=unit_offset, impl=impl, out=fo, **mp)
+            fused(fo)
         f1.record(stream)
         torch.cuda.synchronize()
         fused_ms = shard.max_over_ranks([f0.elapsed_time(f1) / args.steps], device=dev)[0]
@@ -533,8 +540,9 @@ def main():
                        "rows_refined_fp64": refined,
                        "probe_gflop": probe_flop(BH, N, d) / 1e9},
             "ms_mask": mask_ms, "ms_attn": attn_ms, "ms_per_step_two_calls": ms_two_calls,
-            "step_api": ("blade_asa_fwd (one call; attention a programmatic dependent of the "
-                         "mask's last kernel)" if fused_ms is not None else
+            "step_api": (("blade_asa_gt_fwd" if gt else "blade_asa_fwd") +
+                         " (one call; attention a programmatic dependent of the mask's last "
+                         "kernel)" if fused_ms is not None else
                          "blade_asa_mask + blade_bsa_fwd"),
             "clocks": clocks, "e2e": e2e, "roofline": roof, "mask_roofline": mask_roof,
             "cpu_baseline": cpu,

@@ -240,6 +240,23 @@ blade_status_t blade_bsa_gt_bwd(const void* q, const void* k, const void* v, con
                                 void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * blade_asa_gt_fwd — the whole ASA_GT forward in one call (P:135 with
+ * P:138-156): blade_gt_pool, blade_asa_mask, then the attention over the kept
+ * blocks and the global tokens launched as a programmatic dependent of the
+ * mask's last kernel (as blade_asa_fwd).  Results equal blade_gt_pool +
+ * blade_asa_mask + blade_bsa_gt_fwd.
+ *   kg, vg      [BH, N_g, d] bf16 device OUT (N_g = ceil(N/window)): the pooled
+ *               tokens, kept for blade_bsa_gt_bwd.
+ *   window      n >= 1.  Other arguments as blade_asa_fwd (same workspace
+ *               size, blade_asa_fwd_workspace_size); impl MMA_SYNC: UNSUPPORTED.
+ */
+blade_status_t blade_asa_gt_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                                int32_t N, int32_t d, const blade_asa_params_t* params,
+                                int32_t window, int32_t impl, int32_t* kv_idx, int32_t* kv_cnt,
+                                void* kg, void* vg, void* o, float* lse, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/*
  * Locality-preserving token rearrangement ("Gilbert space-filling
  * curve to reorder the tokens before blocking"; Alg. 1 l.1; readings
  * R-21/R-22): video tokens of a t x h x w latent grid (raster order, after

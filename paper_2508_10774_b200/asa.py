@@ -33,7 +33,7 @@ ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd
                "blade_bsa_fwd", "blade_asa_fwd_workspace_size", "blade_asa_fwd",
                "blade_bsa_bwd_workspace_size", "blade_bsa_bwd",
                "blade_gt_pool", "blade_bsa_gt_fwd",
-               "blade_bsa_gt_bwd_workspace_size", "blade_bsa_gt_bwd",
+               "blade_bsa_gt_bwd_workspace_size", "blade_bsa_gt_bwd", "blade_asa_gt_fwd",
                "blade_gilbert_order", "blade_permute_tokens",
                "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
                "blade_status_string", "blade_version")
@@ -81,6 +81,9 @@ _lib.blade_bsa_gt_bwd_workspace_size.argtypes = [_i64, _i32, _i32, _i32, _i32]
 _lib.blade_bsa_gt_bwd.restype = ctypes.c_int
 _lib.blade_bsa_gt_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i32, _i32,
                                   _i32, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+_lib.blade_asa_gt_fwd.restype = ctypes.c_int
+_lib.blade_asa_gt_fwd.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, ctypes.POINTER(BladeAsaParams),
+                                  _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.blade_gilbert_order.restype = ctypes.c_int
 _lib.blade_gilbert_order.argtypes = [_i32, _i32, _i32, _i32, _vp, _i64]
 _lib.blade_permute_tokens.restype = ctypes.c_int
@@ -360,13 +363,14 @@ def blade_bsa_gt_bwd(q, k, v, kg, vg, o, lse, do, kv_idx, kv_cnt, *, window: int
 
 def asa_gt_forward(q, k, v, *, window: int = 128, tau: float = 0.9, keep_min: int = 1,
                    keep_max: int = 1 << 30, samples: int = 16, seed: int = 42,
-                   unit_offset: int = 0, stream=None, **mask_kw):
+                   unit_offset: int = 0, impl: int = ATTN_AUTO, stream=None, **mask_kw):
     """ASA_GT forward: MeanPool_n, mask generation (Alg. 1, unchanged by the
     global tokens, reading R-20), then attention.  Returns (O, LSE, MaskOut)."""
     kg, vg = blade_gt_pool(k, v, window=window, stream=stream)
     m = blade_asa_mask(q, k, tau=tau, keep_min=keep_min, keep_max=keep_max, samples=samples,
                        seed=seed, unit_offset=unit_offset, stream=stream, **mask_kw)
-    o, lse = blade_bsa_gt_fwd(q, k, v, m.kv_idx, m.kv_cnt, kg, vg, window=window, stream=stream)
+    o, lse = blade_bsa_gt_fwd(q, k, v, m.kv_idx, m.kv_cnt, kg, vg, window=window, impl=impl,
+                              stream=stream)
     return o, lse, m
 
 
@@ -470,6 +474,40 @@ def blade_asa_fwd(q, k, v, *, tau: float = 0.9, keep_min: int = 1, keep_max: int
     if st != BLADE_OK:
         raise BladeError(st, "blade_asa_fwd")
     return o, lse, kv_idx, kv_cnt
+
+
+def blade_asa_gt_fwd(q, k, v, *, window: int = 128, tau: float = 0.9, keep_min: int = 1,
+                     keep_max: int = 1 << 30, samples: int = 16, seed: int = 42,
+                     unit_offset: int = 0, impl: int = ATTN_AUTO, want_lse: bool = True,
+                     out=None, stream=None, **mask_kw):
+    """The whole ASA_GT forward in one C call (MeanPool_n, mask, attention over
+    the kept blocks and the global tokens as a programmatic dependent launch).
+    Returns (O, LSE, kv_idx, kv_cnt, K_g, V_g); ``out`` = that tuple to reuse."""
+    q = _as_units(q, "q")
+    k = _as_units(k, "k")
+    v = _as_units(v, "v")
+    BH, N, d = q.shape
+    prm = make_params(d=d, tau=tau, keep_min=keep_min, keep_max=keep_max, samples=samples,
+                      seed=seed, unit_offset=unit_offset, **mask_kw)
+    Nb, Ng = num_blocks(N), num_global_tokens(N, window)
+    if out is None:
+        out = (torch.empty_like(q),
+               torch.empty((BH, N), dtype=torch.float32, device=q.device) if want_lse else None,
+               torch.empty((BH, Nb, Nb), dtype=torch.int32, device=q.device),
+               torch.empty((BH, Nb), dtype=torch.int32, device=q.device),
+               torch.empty((BH, Ng, d), dtype=torch.bfloat16, device=q.device),
+               torch.empty((BH, Ng, d), dtype=torch.bfloat16, device=q.device))
+    o, lse, kv_idx, kv_cnt, kg, vg = out
+    nbytes = _lib.blade_asa_fwd_workspace_size(BH, N, d, ctypes.byref(prm))
+    if nbytes == 0:
+        raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_asa_fwd_workspace_size")
+    ws = _workspace(nbytes, q.device, "fwd")
+    st = _lib.blade_asa_gt_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, ctypes.byref(prm), window,
+                               impl, _ptr(kv_idx), _ptr(kv_cnt), _ptr(kg), _ptr(vg), _ptr(o),
+                               _ptr(lse), _ptr(ws), ws.numel(), _stream(stream))
+    if st != BLADE_OK:
+        raise BladeError(st, "blade_asa_gt_fwd")
+    return o, lse, kv_idx, kv_cnt, kg, vg
 
 
 def asa_forward(q, k, v, *, tau: float = 0.9, keep_min: int = 1, keep_max: int = 1 << 30,

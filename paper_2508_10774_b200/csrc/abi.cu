@@ -148,14 +148,20 @@ size_t blade_asa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d,
   return blade::align256(m) + blade::align256(a) + blade::align256(size_t(BH) * Nb * 4);
 }
 
-blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_t BH,
-                             int32_t N, int32_t d, const blade_asa_params_t* params,
-                             int32_t impl, int32_t* kv_idx, int32_t* kv_cnt, void* o,
-                             float* lse, void* workspace, size_t workspace_bytes,
-                             void* stream) {
+}  // extern "C"
+
+namespace {
+// blade_asa_fwd and blade_asa_gt_fwd (gt != nullptr: kg / vg are pooled here
+// and attended as the global-token tiles)
+blade_status_t asa_fwd_common(const void* q, const void* k, const void* v, int64_t BH, int32_t N,
+                              int32_t d, const blade_asa_params_t* params, int32_t impl,
+                              int32_t* kv_idx, int32_t* kv_cnt, void* o, float* lse,
+                              void* workspace, size_t workspace_bytes, void* stream,
+                              const blade::GtProblem* gt) {
   if (!q || !k || !v || !kv_idx || !kv_cnt || !o) return BLADE_ERR_INVALID_ARG;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
   if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
+  if (gt && impl == BLADE_ATTN_MMA_SYNC) return BLADE_ERR_UNSUPPORTED;
   MaskProblem mp;
   blade_status_t st = make_mask_problem(BH, N, d, params, &mp);
   if (st != BLADE_OK) return st;
@@ -166,6 +172,12 @@ blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_
   const size_t mws = blade::align256(blade::mask_workspace_layout(mp).total);
   char* ws = static_cast<char*>(workspace);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (gt) {  // MeanPool_n of K and V, independent of the mask
+    e = blade::launch_gt_pool(k, v, BH, N, d, gt->window, const_cast<void*>(gt->kg),
+                              const_cast<void*>(gt->vg), s);
+    if (e != cudaSuccess) return BLADE_ERR_CUDA;
+  }
   // programmatic dependent launch of the attention behind K-mask.4 (tcgen05
   // kernels only): rows K-mask.4 recomputes carry a provisional negative
   // count, and only their CTAs wait for it (SURVEY F4 "fused mask->attention")
@@ -181,22 +193,46 @@ blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_
     mp.lpt_order = order;
     mp.lpt_pairs = pair ? 1 : 0;
   }
-  cudaError_t e = blade::launch_mask(mp, q, k, nullptr, kv_idx, kv_cnt, nullptr, nullptr, nullptr,
-                                     ws, s);
+  e = blade::launch_mask(mp, q, k, nullptr, kv_idx, kv_cnt, nullptr, nullptr, nullptr, ws, s);
   if (e != cudaSuccess) return BLADE_ERR_CUDA;
   AttnProblem ap{BH, N, d, mp.b, mp.Nb, mp.scale};
   if (impl == BLADE_ATTN_MMA_SYNC) {
     e = blade::launch_attn_mma(ap, q, k, v, kv_idx, kv_cnt, o, lse, s);
   } else if (impl == BLADE_ATTN_TCGEN05_TRIPLE) {
-    e = blade::launch_attn_tc3(ap, q, k, v, kv_idx, kv_cnt, o, lse, s);
+    e = blade::launch_attn_tc3(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, gt);
   } else if (pair) {
-    e = blade::launch_attn_tc2(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, nullptr, true, order);
+    e = blade::launch_attn_tc2(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, gt, true, order);
   } else {
-    e = blade::launch_attn_tc(ap, q, k, v, kv_idx, kv_cnt, o, lse, ws + mws, aws, s, nullptr,
-                              true, order);
+    e = blade::launch_attn_tc(ap, q, k, v, kv_idx, kv_cnt, o, lse, ws + mws, aws, s, gt, true,
+                              order);
   }
   if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" {
+
+blade_status_t blade_asa_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                             int32_t N, int32_t d, const blade_asa_params_t* params,
+                             int32_t impl, int32_t* kv_idx, int32_t* kv_cnt, void* o,
+                             float* lse, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  return asa_fwd_common(q, k, v, BH, N, d, params, impl, kv_idx, kv_cnt, o, lse, workspace,
+                        workspace_bytes, stream, nullptr);
+}
+
+blade_status_t blade_asa_gt_fwd(const void* q, const void* k, const void* v, int64_t BH,
+                                int32_t N, int32_t d, const blade_asa_params_t* params,
+                                int32_t window, int32_t impl, int32_t* kv_idx, int32_t* kv_cnt,
+                                void* kg, void* vg, void* o, float* lse, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (!kg || !vg || !aligned16(kg) || !aligned16(vg) || window < 1 || BH > 65535)
+    return BLADE_ERR_INVALID_ARG;
+  if (N < 1) return BLADE_ERR_INVALID_ARG;
+  const blade::GtProblem g{kg, vg, int((int64_t(N) + window - 1) / window), int(window)};
+  return asa_fwd_common(q, k, v, BH, N, d, params, impl, kv_idx, kv_cnt, o, lse, workspace,
+                        workspace_bytes, stream, &g);
 }
 
 blade_status_t blade_gt_pool(const void* k, const void* v, int64_t BH, int32_t N, int32_t d,

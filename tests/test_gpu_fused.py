@@ -54,3 +54,26 @@ def test_fused_edges_lpt(A, N, d):
         assert torch.equal(cnt, m.kv_cnt) and torch.equal(idx, m.kv_idx)
         assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
         assert torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("guard", [0.0, 1e30])
+@pytest.mark.parametrize("N,d,n,impl", [(2000, 128, 128, 0), (2000, 64, 100, 0), (1407, 128, 7, 1),
+                                        (300, 64, 1000, 3), (2000, 128, 128, 4)])
+def test_fused_gt_equals_separate_calls(A, N, d, n, impl, guard):
+    """blade_asa_gt_fwd (MeanPool_n + mask + ASA_GT attention, PDL) equals
+    blade_gt_pool + blade_asa_mask + blade_bsa_gt_fwd bit for bit; the MMA_SYNC
+    impl is UNSUPPORTED for the global tokens."""
+    q, k, v = inputs.smooth(1, 2, N, d, (1, 1, N), ell=3.0, beta=9.0, seed=N + d)
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    kw = dict(tau=0.85, keep_min=1, refine_guard=guard)
+    o1, l1, m = A.asa_gt_forward(qd, kd, vd, window=n, impl=impl, **kw)
+    kg1, vg1 = A.blade_gt_pool(kd, vd, window=n)
+    o2, l2, idx, cnt, kg2, vg2 = A.blade_asa_gt_fwd(qd, kd, vd, window=n, impl=impl, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(cnt, m.kv_cnt) and torch.equal(idx, m.kv_idx)
+    assert torch.equal(kg1, kg2) and torch.equal(vg1, vg2)
+    assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+    assert torch.equal(l1, l2)
+    with pytest.raises(A.BladeError) as e:
+        A.blade_asa_gt_fwd(qd, kd, vd, window=n, impl=A.ATTN_MMA_SYNC, **kw)
+    assert e.value.status == A.BLADE_ERR_UNSUPPORTED
