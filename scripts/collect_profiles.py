@@ -72,6 +72,13 @@ def main():
         d = dram(p)
         traffic[wl] = {("attn" if k.startswith("attn") else k.replace("_kernel", "")): v
                        for k, v in d.items()}
+    for wl in ("wan", "cog"):  # backward kernels (F3), not part of the bench roofline
+        p = os.path.join(SRC, f"full_bwd_{wl}.ncu-rep")
+        if os.path.exists(p):
+            summ = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"),
+                                   p], capture_output=True, text=True).stdout
+            open(os.path.join(DST, f"{tag}_ncu_full_bwd_{wl}.txt"), "w").write(summ)
+            traffic[f"bwd_{wl}"] = {k.replace("_kernel", ""): v for k, v in dram(p).items()}
     json.dump(traffic, open(os.path.join(DST, "traffic.json"), "w"), indent=1)
     print(json.dumps(traffic, indent=1))
 
