@@ -54,8 +54,20 @@ struct Cfg2 {
   static constexpr int kTile = 128 * D * 2;  // one Q / K / V tile
   static constexpr int kPanels = D / 64;     // 128-byte SW128 panels along d
   static constexpr int kPanel = 128 * 128;
-  static constexpr int kRingK = D == 128 ? 3 : 5;
-  static constexpr int kRingV = D == 128 ? 2 : 4;
+#ifndef BLADE_ATTN2_RINGK128
+#define BLADE_ATTN2_RINGK128 3  // 2 / 3 within noise on the Wan layer
+#endif
+#ifndef BLADE_ATTN2_RINGV128
+#define BLADE_ATTN2_RINGV128 2
+#endif
+#ifndef BLADE_ATTN2_RINGK64
+#define BLADE_ATTN2_RINGK64 6  // 6 / 6 for d = 64: Cog 1.0358 vs 1.0404 ms (5 / 4), 1.0372 (4 / 3)
+#endif
+#ifndef BLADE_ATTN2_RINGV64
+#define BLADE_ATTN2_RINGV64 6
+#endif
+  static constexpr int kRingK = D == 128 ? BLADE_ATTN2_RINGK128 : BLADE_ATTN2_RINGK64;
+  static constexpr int kRingV = D == 128 ? BLADE_ATTN2_RINGV128 : BLADE_ATTN2_RINGV64;
   static constexpr int kOffQ = 0;  // Q_A, Q_B
   static constexpr int kOffRingK = 2 * kTile;
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
