@@ -27,9 +27,13 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   * attention (A9)   - torch scaled_dot_product_attention (fp64) with the
                        block mask expanded to a boolean token mask; LSE vs
                        torch.logsumexp; V=1 => O=1; V=0 => O=0; V=I => O=P.
-Every function of this module has at least one pin; none is "parity unpinned"
-except the end-to-end composition sample -> probe -> select, which the paper
-gives no worked example for.
+  * composed mask    - asa_mask (Alg. 1) with k = b equals torch
+                       dense softmax + max_pool2d(ceil_mode) followed
+                       by a brute-force selection (math.fsum, numpy lexsort);
+                       with k = 16 it equals the library probe on the
+                       KAT-pinned samples of the global unit index followed
+                       by the same selection (tests/test_oracle_mask_pin.py).
+Every function of this module has at least one pin; none is "parity unpinned".
 """
 
 from __future__ import annotations
@@ -299,9 +303,12 @@ def select_row(p_row: np.ndarray, tau: float, lo: int, hi: int) -> RowSelection:
 
 
 def clamp_bounds(Nb: int, p: AsaParams) -> tuple[int, int]:
-    lo = max(1, min(p.keep_min, Nb))
-    hi = max(lo, min(p.keep_max, Nb))
-    return lo, hi
+    """Integer clamps of Alg. 1 l.9 (reading R-6).  keep_min < 1 or
+    keep_max < keep_min is an argument error (as at the C ABI); values above
+    N_b clip to N_b."""
+    if p.keep_min < 1 or p.keep_max < p.keep_min:
+        raise ValueError(f"need 1 <= keep_min <= keep_max, got {p.keep_min}, {p.keep_max}")
+    return min(p.keep_min, Nb), min(p.keep_max, Nb)
 
 
 # ---------------------------------------------------------------------------
