@@ -87,11 +87,15 @@ size_t blade_asa_mask_workspace_size(int64_t BH, int32_t N, int32_t d,
  *               fp64 (refined) hold that fp64 value rounded to fp32.
  *   sample_idx  [BH, 2, N_b, k] int32 (optional): in-block offsets of the
  *               sampled Q ([:,0]) and K ([:,1]) rows, ascending, -1 padded.
- *               OUTPUT for sample_mode 0/1; INPUT (required) for mode 2.
+ *               OUTPUT for sample_mode 0/1; INPUT (required) for mode 2:
+ *               block i's first k_i = min(k, valid_i) entries must be
+ *               distinct offsets in [0, valid_i) (not checked; other values
+ *               give undefined results, possibly out-of-range reads).
  *   n_refined   device int32 scalar out (optional): rows recomputed in fp64.
  * Errors: INVALID_ARG (NULL q/k/kv_idx/kv_cnt, N < 1, BH < 1, tau out of
  * (0, 1], lo < 1, hi < lo, k < 1 or k > b, reserved != 0, mode 2 without
- * sample_idx), UNSUPPORTED (GPU limits), WORKSPACE, CUDA.
+ * sample_idx), UNSUPPORTED (GPU limits: d not 64/128, b != 128, k not in
+ * {16, 32, 64, 128}, N_b > 512, BH > 65535), WORKSPACE, CUDA.
  */
 blade_status_t blade_asa_mask(const void* q, const void* k, int64_t BH, int32_t N,
                               int32_t d, const blade_asa_params_t* params,
@@ -122,7 +126,9 @@ size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t bl
  *               [0, N_b), 1 <= kv_cnt <= N_b; order is free).
  *   o           [BH, N, d] bf16 out; lse [BH, N] fp32 out (may be NULL).
  *   impl        BLADE_ATTN_* selector.
- * Errors: INVALID_ARG, UNSUPPORTED (GPU limits; impl not built), WORKSPACE, CUDA.
+ * Errors: INVALID_ARG, UNSUPPORTED (GPU limits: d not 64/128, block != 128,
+ * N_b > 512, BH > 65535; impl not built), WORKSPACE, CUDA.  All checks run
+ * before anything is enqueued.
  */
 blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_t BH,
                              int32_t N, int32_t d, int32_t block, float scale,

@@ -131,11 +131,18 @@ def keep_count(ratio_ppm: int, Nb: int) -> int:
 _workspaces: dict = {}
 
 
-def _workspace(nbytes: int, device: torch.device, tag: str) -> torch.Tensor:
-    key = (device, tag)
+def _workspace(nbytes: int, device: torch.device, tag: str, stream=None) -> torch.Tensor:
+    """Scratch for one entry point, cached per (device, tag, stream): two
+    calls on different streams never share scratch (refine queue, Q_s/K_s,
+    LPT order).  The buffer is allocated on ``stream`` (the caching
+    allocator then only recycles it after work queued there), so a regrowth
+    cannot hand memory still in use by an earlier launch to anyone else."""
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    key = (device, tag, s.cuda_stream)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
+        with torch.cuda.stream(s):
+            buf = torch.empty(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
         _workspaces[key] = buf
     off = (-buf.data_ptr()) % 256
     return buf[off:off + max(nbytes, 256)]
@@ -213,7 +220,7 @@ def blade_asa_mask(q: torch.Tensor, k: torch.Tensor, *, tau: float = 0.9, keep_m
                                  _ptr(out.kv_idx), _ptr(out.kv_cnt), None, None, None, None, 0,
                                  None)
         raise BladeError(st if st else BLADE_ERR_INVALID_ARG, "blade_asa_mask")
-    ws = _workspace(nbytes, dev, "mask")
+    ws = _workspace(nbytes, dev, "mask", stream)
     st = _lib.blade_asa_mask(_ptr(q), _ptr(k), BH, N, d, ctypes.byref(prm), _ptr(out.mask),
                              _ptr(out.kv_idx), _ptr(out.kv_cnt), _ptr(out.p_imp),
                              _ptr(out.sample_idx), _ptr(out.n_refined), _ptr(ws), ws.numel(),
@@ -243,7 +250,7 @@ def blade_bsa_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_idx: tor
     nbytes = _lib.blade_bsa_fwd_workspace_size(BH, N, d, block)
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_fwd_workspace_size")
-    ws = _workspace(nbytes, q.device, "attn")
+    ws = _workspace(nbytes, q.device, "attn", stream)
     st = _lib.blade_bsa_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, block,
                             default_scale(d) if scale is None else scale, _ptr(kv_idx),
                             _ptr(kv_cnt), _ptr(o), _ptr(lse), impl, _ptr(ws), ws.numel(),
@@ -267,7 +274,7 @@ def blade_bsa_bwd(q, k, v, o, lse, do, kv_idx, kv_cnt, *, scale: float | None = 
     nbytes = _lib.blade_bsa_bwd_workspace_size(BH, N, d, block)
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_bwd_workspace_size")
-    ws = _workspace(nbytes, q.device, "bwd")
+    ws = _workspace(nbytes, q.device, "bwd", stream)
     st = _lib.blade_bsa_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse.contiguous()), _ptr(do),
                             BH, N, d, block, default_scale(d) if scale is None else scale,
                             _ptr(kv_idx), _ptr(kv_cnt), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws),
@@ -321,7 +328,7 @@ def blade_bsa_gt_fwd(q, k, v, kv_idx, kv_cnt, kg, vg, *, window: int = 128,
     nbytes = _lib.blade_bsa_fwd_workspace_size(BH, N, d, block)
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_fwd_workspace_size")
-    ws = _workspace(nbytes, q.device, "attn")
+    ws = _workspace(nbytes, q.device, "attn", stream)
     st = _lib.blade_bsa_gt_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, block,
                                default_scale(d) if scale is None else scale, _ptr(kv_idx),
                                _ptr(kv_cnt), _ptr(kg), _ptr(vg), window, _ptr(o), _ptr(lse),
@@ -350,7 +357,7 @@ def blade_bsa_gt_bwd(q, k, v, kg, vg, o, lse, do, kv_idx, kv_cnt, *, window: int
     nbytes = _lib.blade_bsa_gt_bwd_workspace_size(BH, N, d, block, window)
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_bsa_gt_bwd_workspace_size")
-    ws = _workspace(nbytes, q.device, "gt_bwd")
+    ws = _workspace(nbytes, q.device, "gt_bwd", stream)
     st = _lib.blade_bsa_gt_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(kg), _ptr(vg), window, _ptr(o),
                                _ptr(lse.contiguous()), _ptr(do), BH, N, d, block,
                                default_scale(d) if scale is None else scale, _ptr(kv_idx),
@@ -436,7 +443,7 @@ def blade_asa_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, tau
     nbytes = _lib.blade_asa_fwd_host_workspace_size(BH, N, d, ctypes.byref(prm), chunk_units)
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_asa_fwd_host_workspace_size")
-    ws = _workspace(nbytes, dev, "host")
+    ws = _workspace(nbytes, dev, "host", stream)
     st = _lib.blade_asa_fwd_host(_ptr(q), _ptr(k), _ptr(v), BH, N, d, ctypes.byref(prm), impl,
                                  chunk_units, _ptr(o), _ptr(lse), _ptr(kv_cnt), _ptr(ws),
                                  ws.numel(), _stream(stream))
@@ -467,7 +474,7 @@ def blade_asa_fwd(q, k, v, *, tau: float = 0.9, keep_min: int = 1, keep_max: int
     nbytes = _lib.blade_asa_fwd_workspace_size(BH, N, d, ctypes.byref(prm))
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_asa_fwd_workspace_size")
-    ws = _workspace(nbytes, q.device, "fwd")
+    ws = _workspace(nbytes, q.device, "fwd", stream)
     st = _lib.blade_asa_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, ctypes.byref(prm), impl,
                             _ptr(kv_idx), _ptr(kv_cnt), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(),
                             _stream(stream))
@@ -501,7 +508,7 @@ def blade_asa_gt_fwd(q, k, v, *, window: int = 128, tau: float = 0.9, keep_min: 
     nbytes = _lib.blade_asa_fwd_workspace_size(BH, N, d, ctypes.byref(prm))
     if nbytes == 0:
         raise BladeError(BLADE_ERR_UNSUPPORTED, "blade_asa_fwd_workspace_size")
-    ws = _workspace(nbytes, q.device, "fwd")
+    ws = _workspace(nbytes, q.device, "fwd", stream)
     st = _lib.blade_asa_gt_fwd(_ptr(q), _ptr(k), _ptr(v), BH, N, d, ctypes.byref(prm), window,
                                impl, _ptr(kv_idx), _ptr(kv_cnt), _ptr(kg), _ptr(vg), _ptr(o),
                                _ptr(lse), _ptr(ws), ws.numel(), _stream(stream))

@@ -15,6 +15,7 @@ using blade::MaskProblem;
 
 constexpr int kGpuBlock = 128;
 constexpr int kMaxNb = 512;
+constexpr int64_t kMaxBH = 65535;  // units ride in gridDim.y of every kernel
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -28,6 +29,7 @@ blade_status_t make_mask_problem(int64_t BH, int32_t N, int32_t d,
   if (!(prm->scale > 0.f) || !isfinite(prm->scale)) return BLADE_ERR_INVALID_ARG;
   if (prm->unit_offset < 0) return BLADE_ERR_INVALID_ARG;
   if (prm->block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  if (BH > kMaxBH) return BLADE_ERR_UNSUPPORTED;
   if (prm->samples != 16 && prm->samples != 32 && prm->samples != 64 && prm->samples != 128)
     return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + prm->block - 1) / prm->block;
@@ -107,7 +109,7 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
   if (BH < 1 || N < 1 || block < 1 || !(scale > 0.f) || !isfinite(scale)) return BLADE_ERR_INVALID_ARG;
   if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
-  if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  if (block != kGpuBlock || (d != 64 && d != 128) || BH > kMaxBH) return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
   AttnProblem p{BH, N, d, block, int(Nb), scale};
@@ -227,8 +229,8 @@ blade_status_t blade_asa_gt_fwd(const void* q, const void* k, const void* v, int
                                 int32_t window, int32_t impl, int32_t* kv_idx, int32_t* kv_cnt,
                                 void* kg, void* vg, void* o, float* lse, void* workspace,
                                 size_t workspace_bytes, void* stream) {
-  if (!kg || !vg || !aligned16(kg) || !aligned16(vg) || window < 1 || BH > 65535)
-    return BLADE_ERR_INVALID_ARG;
+  if (!kg || !vg || !aligned16(kg) || !aligned16(vg) || window < 1) return BLADE_ERR_INVALID_ARG;
+  if (BH > kMaxBH) return BLADE_ERR_UNSUPPORTED;
   if (N < 1) return BLADE_ERR_INVALID_ARG;
   const blade::GtProblem g{kg, vg, int((int64_t(N) + window - 1) / window), int(window)};
   return asa_fwd_common(q, k, v, BH, N, d, params, impl, kv_idx, kv_cnt, o, lse, workspace,
@@ -259,7 +261,8 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
   if (BH < 1 || N < 1 || block < 1 || window < 1 || !(scale > 0.f) || !isfinite(scale))
     return BLADE_ERR_INVALID_ARG;
   if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
-  if (block != kGpuBlock || (d != 64 && d != 128) || impl == BLADE_ATTN_MMA_SYNC)
+  if (block != kGpuBlock || (d != 64 && d != 128) || impl == BLADE_ATTN_MMA_SYNC ||
+      BH > kMaxBH)
     return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
@@ -302,7 +305,7 @@ blade_status_t blade_bsa_bwd(const void* q, const void* k, const void* v, const 
     if (!aligned16(x)) return BLADE_ERR_INVALID_ARG;
   if (BH < 1 || BH > 65535 || N < 1 || block < 1 || !(scale > 0.f) || !isfinite(scale))
     return BLADE_ERR_INVALID_ARG;
-  if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  if (block != kGpuBlock || (d != 64 && d != 128) || BH > kMaxBH) return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
   AttnProblem p{BH, N, d, block, int(Nb), scale};
@@ -339,7 +342,7 @@ blade_status_t blade_bsa_gt_bwd(const void* q, const void* k, const void* v, con
   if (BH < 1 || BH > 65535 || N < 1 || block < 1 || window < 1 || !(scale > 0.f) ||
       !isfinite(scale))
     return BLADE_ERR_INVALID_ARG;
-  if (block != kGpuBlock || (d != 64 && d != 128)) return BLADE_ERR_UNSUPPORTED;
+  if (block != kGpuBlock || (d != 64 && d != 128) || BH > kMaxBH) return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
   AttnProblem p{BH, N, d, block, int(Nb), scale};

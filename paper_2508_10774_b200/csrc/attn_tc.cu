@@ -163,7 +163,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int i = int(row_id % Nb);
   const int64_t u = row_id / Nb;
   int cnt_fine = kv_cnt[row_id];
-  if (pdl && cnt_fine < 0) {  // refined row (blade_asa_fwd): wait for K-mask.4's final list
+  // a CTA that waited reads its list through L2 (ld.global.cg): see attn_tc2.cu
+  const bool waited = pdl && cnt_fine < 0;
+  auto ld_list = [waited](const int32_t* p) { return waited ? __ldcg(p) : __ldg(p); };
+  if (waited) {  // refined row (blade_asa_fwd): wait for K-mask.4's final list
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     cnt_fine = __ldcg(kv_cnt + row_id);
   }
@@ -222,10 +225,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ahead of the ring: a block's first touch comes from HBM
       for (int n = 0; n < BLADE_ATTN_L2_PREFETCH && n < cnt_fine; ++n)
         for (int p = 0; p < C::kPanels; ++p) tc::tma_prefetch_3d(m, p * 64, list[n] * 128, int(u));
-      int jn = cnt_fine > 0 ? __ldg(list) : 0;  // block id, loaded one item ahead
+      int jn = cnt_fine > 0 ? ld_list(list) : 0;  // block id, loaded one item ahead
       for (int n = 0; n < cnt; ++n) {
         const int jb = jn;
-        if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
+        if (n + 1 < cnt_fine) jn = ld_list(list + n + 1);
         const int s = n % R;
         TC_DBG(0, n);
         if (BLADE_ATTN_L2_PREFETCH > 0 && n + BLADE_ATTN_L2_PREFETCH < cnt_fine)
@@ -359,11 +362,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc::mbar_arrive(bar_qt);
     }
     float m_used = -INFINITY, l_sum = 0.f;
-    int jn = cnt_fine > 0 ? __ldg(list) : 0;  // block id, loaded one tile ahead
+    int jn = cnt_fine > 0 ? ld_list(list) : 0;  // block id, loaded one tile ahead
     for (int n = 0; n < cnt; ++n) {
       const int buf = n & 1;
       const int jb = jn;
-      if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
+      if (n + 1 < cnt_fine) jn = ld_list(list + n + 1);
       const uint32_t tS = tmem + lane_base + buf * 128;
       if (lane == 0) TC_DBG(2 + (warp & 3), 10 * n + 1);
 #ifdef BLADE_ATTN_TIMING

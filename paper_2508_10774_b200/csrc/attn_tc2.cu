@@ -180,7 +180,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int ngt = kGT ? (gt.Ng + 127) / 128 : 0;
   int cf0 = kv_cnt[u * Nb + i0];
   int cf1 = nblk == 2 ? kv_cnt[u * Nb + i0 + 1] : 0;
-  if (pdl && (cf0 < 0 || cf1 < 0)) {  // a refined row (blade_asa_fwd): wait for K-mask.4
+  // a CTA that waited reads its lists through L2 (ld.global.cg): the refine
+  // kernel rewrote them while this grid ran, and a line another CTA on this
+  // SM pulled into L1 through the non-coherent path before could be stale
+  const bool waited = pdl && (cf0 < 0 || cf1 < 0);
+  auto ld_list = [waited](const int32_t* p) { return waited ? __ldcg(p) : __ldg(p); };
+  if (waited) {  // a refined row (blade_asa_fwd): wait for K-mask.4
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     cf0 = __ldcg(kv_cnt + u * Nb + i0);
     cf1 = nblk == 2 ? __ldcg(kv_cnt + u * Nb + i0 + 1) : 0;
@@ -244,14 +249,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
       int g = 0;
       // the next block id of each list is loaded one item ahead, so the L2
       // latency of the list read overlaps the wait for a free slot
-      int pre0 = cf0 > 0 ? __ldg(list0) : 0, pre1 = cf1 > 0 ? __ldg(list1) : 0;
+      int pre0 = cf0 > 0 ? ld_list(list0) : 0, pre1 = cf1 > 0 ? ld_list(list1) : 0;
       for_each_item(cnt0, cnt1, [&](int t, int k) {
         const int cf = t ? cf1 : cf0;
         const bool fine = !kGT || k < cf;
         const int jb = t ? pre1 : pre0;
         if (k + 1 < cf) {
-          if (t) pre1 = __ldg(list1 + k + 1);
-          else pre0 = __ldg(list0 + k + 1);
+          if (t) pre1 = ld_list(list1 + k + 1);
+          else pre0 = ld_list(list0 + k + 1);
         }
         const int s = g % R;
         tc::mbar_wait(empty + s, ((g / R) & 1) ^ 1);
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const uint32_t tO = tmem + lane_base + C::kColO + t * D;
     const int r = qw * 32 + lane;
     float m_used = -INFINITY, l_sum = 0.f;
-    int jn = cnt_fine > 0 ? __ldg(list) : 0;  // block id, loaded one tile ahead
+    int jn = cnt_fine > 0 ? ld_list(list) : 0;  // block id, loaded one tile ahead
     if constexpr (C::kHalfS) {
       const float2 sl2 = make_float2(scale_log2, scale_log2);
       // rescale O_t (and l) by f; O_t must be current
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       };
       for (int n = 0; n < cnt; ++n) {
         const int jb = jn;
-        if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
+        if (n + 1 < cnt_fine) jn = ld_list(list + n + 1);
         const uint32_t E = tS + (n & 1) * 64, Lc = tS + ((n & 1) ^ 1) * 64;
         float x[64];
         // ---- early half (keys [0, 64)) in E_n
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     } else
     for (int n = 0; n < cnt; ++n) {
       const int jb = jn;
-      if (n + 1 < cnt_fine) jn = __ldg(list + n + 1);
+      if (n + 1 < cnt_fine) jn = ld_list(list + n + 1);
       tc::mbar_wait(bar_s + t, n & 1);
       tc::fence_after_sync();
       if (lane == 0 && qw == 0) TR2(6 + t, n);

@@ -121,7 +121,7 @@ blade_status_t blade_asa_fwd_host(const void* q_host, const void* k_host, const 
                                   int32_t* kv_cnt_host, void* workspace,
                                   size_t workspace_bytes, void* stream) {
   if (!q_host || !k_host || !v_host || !o_host || !params) return BLADE_ERR_INVALID_ARG;
-  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_MMA_SYNC) return BLADE_ERR_INVALID_ARG;
+  if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
   HostWs w;
   int64_t C;
   if (!sizes(BH, N, d, params, chunk_units, &w, &C)) {

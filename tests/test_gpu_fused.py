@@ -77,3 +77,23 @@ def test_fused_gt_equals_separate_calls(A, N, d, n, impl, guard):
     with pytest.raises(A.BladeError) as e:
         A.blade_asa_gt_fwd(qd, kd, vd, window=n, impl=A.ATTN_MMA_SYNC, **kw)
     assert e.value.status == A.BLADE_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("d,impl", [(128, 0), (64, 0), (128, 1)])
+def test_fused_many_ctas_mixed_refined_rows(A, d, impl):
+    """More CTAs than SMs, a small N_b (several rows share one 128-B line of
+    kv_idx) and a mix of refined and unrefined rows: CTAs that waited for the
+    refine kernel must read their rewritten lists, not a stale L1 line pulled
+    in by a CTA that did not wait (coherent list loads)."""
+    q, k, v = inputs.smooth(1, 32, 1000, d, (1, 1, 1000), ell=3.0, beta=9.0, seed=77 + d)
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    kw = dict(tau=0.9, keep_min=1, refine_guard=1e-3)
+    o1, l1, m = A.asa_forward(qd, kd, vd, impl=impl, **kw)
+    n_ref = int(m.n_refined.item())
+    assert 0 < n_ref < 32 * 8, n_ref
+    for _ in range(3):
+        o2, l2, idx, cnt = A.blade_asa_fwd(qd, kd, vd, impl=impl, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(cnt, m.kv_cnt) and torch.equal(idx, m.kv_idx)
+        assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+        assert torch.equal(l1, l2)
