@@ -2,23 +2,31 @@
 """Benchmark of the B200-native ASA forward (BLADE, arXiv 2508.10774).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl blade|reference]
-                    [--workload wan|cog|tiny] [--keep 51 | --tau-mode] [--attn auto|tcgen05|mma]
+                    [--workload wan|cog|tiny|wan_stack] [--keep 51 | --tau-mode]
 
 One STEP = one pass of the whole hot path (mask
-generation, then block-sparse attention) over one batch: at N=1 the
-Wan2.1-1.3B single attention layer of BASELINE.json configs[1]
-(B=1, H=12, N=32760, d=128, bf16, smooth-field synthetic inputs,
-keep-ratio 51/256 = sparsity 0.801 by default).  At N GPUs the batch is N
-samples (units sharded by (batch, head), one sample per rank, no collective
-on the data path): "scaling": "weak".
+generation, then block-sparse attention) over one batch of synthetic input.
+
+N = 1 (default): the Wan2.1-1.3B single attention layer of BASELINE.json
+    configs[1] (B=1, H=12, N=32760, d=128, bf16, smooth-field inputs,
+    keep-ratio 51/256 = sparsity 0.801).  The step is the production single
+    call ``blade_asa_fwd``; the same K steps as two calls (``blade_asa_mask``
+    + ``blade_bsa_fwd``) give the mask / attention split.  The line also
+    carries, as sub-objects, the CogVideoX-5B layer (configs[2]), a sustained
+    (~2 s continuous) run of the headline call, and the configs[4] stack on
+    one GPU (the N = 1 point of the strong-scaling curve).
+N > 1: BASELINE.json configs[4], strong scaling: the Wan2.1-1.3B attention
+    stack, batch 8 x 30 layers, 96 (batch, head) units split over the ranks
+    (contiguous unit ranges, ``unit_offset`` keys the sampler, inputs seeded
+    per GLOBAL unit, so every N computes identical tensors), ``blade_asa_fwd``
+    per layer, and the last layer's O gathered to rank 0 over NCCL inside the
+    timed step.  ``bench.py --gpus N`` launches its own N ranks (torchrun,
+    127.0.0.1) when it is not already running under torchrun.
 
 metric  = BASELINE.json metric: active-block TFLOP/s of the whole ASA call
           (active FLOP = 4 d sum over kept (i,j) valid_i valid_j, probe FLOP
-          excluded) and ms per call; value = all ranks' active FLOP / max
-          over ranks of the device time of the production single call
-          blade_asa_fwd (K steps, CUDA events); the same K steps as two calls
-          (blade_asa_mask + blade_bsa_fwd, an event between them) give the
-          mask / attention split (ms_mask, ms_attn) and ms_per_step_two_calls.
+          excluded); value = all ranks' active FLOP / (max over ranks of the
+          device time of the K timed steps / K).
 e2e     = the same metric through the C ABI with host buffers: pinned host
           Q/K/V -> device, ASA forward, O + LSE -> pinned host, every step.
 roofline = attention kernel (the dominant kernel) against the measured bf16
@@ -31,6 +39,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -51,10 +60,11 @@ METRIC = "ASA fwd ms/call and effective TFLOPS (active blocks) vs bf16 peak at 1
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
-    ap.add_argument("--workload", default="wan", choices=["wan", "cog", "tiny", "wan_stack"])
+    ap.add_argument("--workload", default=None, choices=["wan", "cog", "tiny", "wan_stack"],
+                    help="default: wan at N=1, wan_stack at N>1")
     ap.add_argument("--layers", type=int, default=30, help="wan_stack: attention layers per step")
     ap.add_argument("--keep", type=int, default=None,
                     help="keep-ratio mode: lo = hi = KEEP blocks per row (default 51 wan / 25 cog)")
@@ -68,8 +78,9 @@ def parse():
     ap.add_argument("--e2e-chunk", type=int, default=0,
                     help="units per chunk of the host-buffer pipeline (0 = library default)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--gather", action="store_true",
-                    help="after timing, NCCL-gather every rank's O to rank 0 (BJ configs[4])")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="N=1: skip the cog / sustained / stack sub-measurements")
+    ap.add_argument("--sustained-s", type=float, default=2.0)
     return ap.parse_args()
 
 
@@ -80,11 +91,27 @@ def dist_env():
     return ws, rank, local
 
 
-def mask_params(w, args, Nb):
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks of this script."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def mask_params(args, workload: str, Nb: int):
     if args.tau_mode:
         return dict(tau=args.tau, keep_min=max(1, -(-5 * Nb // 100)), keep_max=Nb), "tau"
     keep = args.keep if args.keep is not None else {"wan": 51, "cog": 25, "tiny": 2,
-                                                    "wan_stack": 51}[args.workload]
+                                                    "wan_stack": 51}[workload]
     keep = min(keep, Nb)
     return dict(tau=args.tau, keep_min=keep, keep_max=keep), f"keep{keep}"
 
@@ -93,12 +120,9 @@ def active_flop(kv_idx: np.ndarray, kv_cnt: np.ndarray, N: int, d: int, b: int =
     """4 d sum_{u, kept (i, j)} valid_i valid_j."""
     Nb = kv_cnt.shape[1]
     valid = np.array([min(b, N - i * b) for i in range(Nb)], dtype=np.float64)
-    total = 0.0
-    for u in range(kv_cnt.shape[0]):
-        for i in range(Nb):
-            idx = kv_idx[u, i, :kv_cnt[u, i]]
-            total += valid[i] * valid[idx].sum()
-    return 4.0 * d * total
+    live = np.arange(Nb)[None, None, :] < kv_cnt[:, :, None]
+    cols = np.where(live, valid[np.clip(kv_idx, 0, Nb - 1)], 0.0).sum(-1)   # [BH, Nb]
+    return 4.0 * d * float((cols * valid[None, :]).sum())
 
 
 def probe_flop(BH, N, d, k=16, b=128):
@@ -164,39 +188,6 @@ def traffic_for(workload: str, kernel: str):
         return None
 
 
-# ---------------------------------------------------------------------------
-# CPU oracle legs (the only place bench.py touches oracle/)
-# ---------------------------------------------------------------------------
-
-
-def oracle_sample(q, k, v, w, mp, units: int, qblocks: int | None):
-    """Time the fp64 oracle (as it stands) on `units` units: the full mask and
-    the attention of `qblocks` evenly spaced query blocks per unit (all if
-    None).  Returns (active FLOP of the sampled units' full calls, seconds
-    for those full calls, description); with a subset of query blocks the
-    attention seconds are scaled by active FLOP to the whole unit."""
-    from oracle import asa_oracle as O
-    p = O.AsaParams(tau=mp["tau"], keep_min=mp["keep_min"], keep_max=mp["keep_max"])
-    t0 = time.perf_counter()
-    r = O.asa_mask(q[:units], k[:units], p)
-    t_mask = time.perf_counter() - t0
-    Nb = r.kv_cnt.shape[1]
-    blocks = (list(range(Nb)) if qblocks is None else
-              sorted(set(np.linspace(0, Nb - 1, qblocks).astype(int).tolist())))
-    t0 = time.perf_counter()
-    O.sparse_attention(q[:units], k[:units], v[:units], r.kv_idx, r.kv_cnt, 128, qblocks=blocks)
-    t_att = time.perf_counter() - t0
-    valid = np.array([min(128, w.N - i * 128) for i in range(Nb)], dtype=np.float64)
-    f_blk = lambda u, i: 4.0 * w.d * valid[i] * valid[r.kv_idx[u, i, :r.kv_cnt[u, i]]].sum()
-    f_all = sum(f_blk(u, i) for u in range(units) for i in range(Nb))
-    f_smp = sum(f_blk(u, i) for u in range(units) for i in blocks)
-    secs = t_mask + t_att * f_all / f_smp
-    desc = (f"{units} of {w.B * w.H} units, fp64 numpy oracle: full mask ({t_mask:.2f} s) + "
-            f"attention of {len(blocks)} of {Nb} query blocks per unit ({t_att:.2f} s)"
-            + ("" if qblocks is None else ", attention time scaled by active FLOP to all blocks"))
-    return f_all, secs, desc
-
-
 def cores_used() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -204,36 +195,74 @@ def cores_used() -> int:
         return os.cpu_count() or 1
 
 
+# ---------------------------------------------------------------------------
+# CPU oracle legs (the only place bench.py touches oracle/)
+# ---------------------------------------------------------------------------
+
+
+def oracle_sample(q, k, v, N, d, mp, units, qblocks: int | None):
+    """Time the fp64 oracle (as it stands) on the first ``units`` units: their
+    full mask and the attention of ``qblocks`` evenly spaced query blocks
+    per unit (all if None).  Returns (active FLOP of the attention actually
+    run, seconds it took, description, mask seconds, attention seconds per
+    query block) — no extrapolation."""
+    from oracle import asa_oracle as O
+    p = O.AsaParams(tau=mp["tau"], keep_min=mp["keep_min"], keep_max=mp["keep_max"])
+    t0 = time.perf_counter()
+    r = O.asa_mask(q[:units], k[:units], p)
+    t_mask = time.perf_counter() - t0
+    Nb = r.kv_cnt.shape[1]
+    blocks = (list(range(Nb)) if qblocks is None or qblocks >= Nb else
+              sorted(set(np.linspace(0, Nb - 1, qblocks).astype(int).tolist())))
+    t0 = time.perf_counter()
+    O.sparse_attention(q[:units], k[:units], v[:units], r.kv_idx, r.kv_cnt, 128, qblocks=blocks)
+    t_att = time.perf_counter() - t0
+    valid = np.array([min(128, N - i * 128) for i in range(Nb)], dtype=np.float64)
+    flop = sum(4.0 * d * valid[i] * valid[r.kv_idx[u, i, :r.kv_cnt[u, i]]].sum()
+               for u in range(units) for i in blocks)
+    desc = (f"{units} unit(s) of the layer, fp64 numpy oracle: full mask ({t_mask:.2f} s) + "
+            f"attention of {len(blocks)} of {Nb} query blocks per unit ({t_att:.2f} s); value = "
+            "active FLOP of the attention actually run / (mask + attention seconds)")
+    return flop, t_mask + t_att, desc, t_mask, t_att / (units * len(blocks))
+
+
 def run_reference(args, ws, rank):
-    """--impl reference: the oracle as it stands, on bounded samples."""
+    """--impl reference: the oracle as it stands (there is no reference
+    implementation: the reference is a paper), on bounded samples of the same
+    workload and metric.  Each of the W + K steps runs the same sample: one
+    unit's full mask plus the attention of as many of its query blocks as fit
+    a per-step budget that keeps the whole run within ~2-3 minutes; the
+    reported time per step is the time of the work actually run."""
     if rank != 0:
         return
-    w = inputs.WORKLOADS[args.workload]
+    name = args.workload or ("wan" if ws == 1 else "wan_stack")
+    w = inputs.WORKLOADS["wan" if name == "wan_stack" else name]
     q, k, v = inputs.smooth(1, 1, w.N, w.d, w.grid, w.n_text, w.ell, w.beta, w.sigma_n, seed=42)
     Nb = (w.N + 127) // 128
-    mp, mode = mask_params(w, args, Nb)
+    mp, mode = mask_params(args, name, Nb)
+    budget_s = float(os.environ.get("BLADE_REF_BUDGET_S", "150"))
+    per_step = budget_s / max(1, args.steps + args.warmup)
+    # calibrate on a 4-block sample, then size the per-step sample to the budget
+    _, _, _, t_mask, t_blk = oracle_sample(q, k, v, w.N, w.d, mp, 1, 4)
+    qb = int(max(1, min(Nb, (per_step - t_mask) / max(t_blk, 1e-4))))
+    for _ in range(args.warmup):
+        oracle_sample(q, k, v, w.N, w.d, mp, 1, qb)
     vals, secs = [], []
     desc = ""
-    # each step is one bounded sample (~3 s on the Wan layer); the run stops
-    # early once the next step would exceed the time budget, so the arm ends
-    # within a few minutes whatever --steps is (steps_run says how many ran)
-    budget = float(os.environ.get("BLADE_REF_BUDGET_S", "150"))
-    t_start = time.perf_counter()
     for _ in range(args.steps):
-        flop, sec, desc = oracle_sample(q, k, v, w, mp, 1, 8 if args.workload != "tiny" else None)
+        flop, sec, desc, _, _ = oracle_sample(q, k, v, w.N, w.d, mp, 1, qb)
         vals.append(flop / sec / 1e12)
         secs.append(sec)
-        if time.perf_counter() - t_start + sec > budget:
-            break
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d, "mask": mode,
-                   "tau": mp["tau"], "sample_per_step": desc, "steps_run": len(vals),
-                   "time_budget_s": budget},
+        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": w.name if name != "wan_stack" else inputs.WORKLOADS[name].name,
+                   "B": 1, "H": w.H, "N": w.N, "d": w.d, "mask": mode, "tau": mp["tau"],
+                   "sample_per_step": desc, "query_blocks_per_step": qb},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores_used(),
                          "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -267,112 +296,147 @@ def init_dist(dev: torch.device) -> None:
         dist.init_process_group("nccl", device_id=dev)
 
 
-def run_stack(args, ws, rank, local, dev):
+def _ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def time_loop(fn, steps: int, stream) -> float:
+    """Mean ms per call of ``steps`` back-to-back calls (CUDA events on the
+    launching stream)."""
+    e0, e1 = _ev(), _ev()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def stack_layers(w, args, lo: int, hi: int, dev):
+    """Per-layer inputs of the configs[4] stack for GLOBAL units [lo, hi)
+    (seed 42 + layer, one generator per global unit: identical at every N)."""
+    return [inputs.smooth_device(range(lo, hi), w.N, w.d, w.grid, dev, ell=w.ell, beta=w.beta,
+                                 sigma_n=w.sigma_n, seed=42 + layer)
+            for layer in range(args.layers)]
+
+
+def run_stack(args, ws, rank, local, dev, *, sub: bool = False):
     """BASELINE.json configs[4]: the Wan2.1-1.3B attention stack, batch 8 x
     30 layers, (batch, head) units sharded over the ranks (strong scaling:
-    the total work is fixed), per-layer inputs generated on the device
-    before timing, and the last layer's O gathered to rank 0 over NCCL
-    inside the timed step."""
+    the total work is fixed), one ``blade_asa_fwd`` per layer, the last
+    layer's O gathered to rank 0 inside the timed step (NCCL)."""
     from paper_2508_10774_b200 import asa as A
     from paper_2508_10774_b200 import shard
     w = inputs.WORKLOADS["wan_stack"]
     units = w.B * w.H
     lo, hi = shard.unit_range(ws, rank, units)
     Nb = (w.N + 127) // 128
-    mp, mode = mask_params(w, args, Nb)
-    layers = []
-    for layer in range(args.layers):  # seed 42 + layer; each rank draws only its units
-        q, k, v = inputs.smooth_device(hi - lo, w.N, w.d, w.grid, dev, ell=w.ell, beta=w.beta,
-                                       sigma_n=w.sigma_n, seed=(42 + layer) * 1000 + lo)
-        layers.append((q, k, v))
+    mp, mode = mask_params(args, "wan_stack", Nb)
+    layers = stack_layers(w, args, lo, hi, dev)
     stream = torch.cuda.current_stream()
-    o_last = torch.empty_like(layers[0][0])
+    outs = [None]
 
-    def step(gather: bool):
-        m = None
+    def layer_call(li, q, k, v):
+        outs[0] = A.blade_asa_fwd(q, k, v, unit_offset=lo, seed=42 + li, out=outs[0], **mp)
+        return outs[0]
+
+    ev_g = [None]
+
+    def step():
         for li, (q, k, v) in enumerate(layers):
-            m = A.blade_asa_mask(q, k, unit_offset=lo, want_mask=False, seed=42 + li, **mp)
-            A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, o=o_last if li == len(layers) - 1
-                            else None, want_lse=False)
-        if gather and ws > 1:
-            shard.gather_units(o_last, units)
-        return m
+            layer_call(li, q, k, v)
+        if ev_g[0] is not None:
+            ev_g[0].record(stream)
+        if ws > 1:
+            return shard.gather_units(outs[0][0], units)
+        return outs[0][0]
 
     flop = 0.0
     for li, (q, k, v) in enumerate(layers):  # active FLOP of this rank's units, every layer
-        m = A.blade_asa_mask(q, k, unit_offset=lo, want_mask=False, seed=42 + li, **mp)
-        flop += active_flop(m.kv_idx.cpu().numpy(), m.kv_cnt.cpu().numpy(), w.N, w.d)
+        _, _, idx, cnt = layer_call(li, q, k, v)
+        flop += active_flop(idx.cpu().numpy(), cnt.cpu().numpy(), w.N, w.d)
     for _ in range(max(args.warmup, 3)):
-        step(True)
+        step()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = None if sub else ClockSampler(local)
+    e0, e1 = _ev(), _ev()
+    gstarts = [_ev() for _ in range(args.steps)]
+    gends = [_ev() for _ in range(args.steps)]
     e0.record(stream)
-    for _ in range(args.steps):
-        step(True)
+    for s in range(args.steps):
+        ev_g[0] = gstarts[s]
+        step()
+        gends[s].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
-    clocks = clk.stop()
-    ms = shard.max_over_ranks([e0.elapsed_time(e1) / args.steps], device=dev)[0]
+    clocks = clk.stop() if clk else None
+    ms_local = e0.elapsed_time(e1) / args.steps
+    gather_ms_local = statistics.mean(gstarts[s].elapsed_time(gends[s]) for s in range(args.steps))
+    ms, gather_ms = shard.max_over_ranks([ms_local, gather_ms_local], device=dev)
     flop_all = shard.sum_over_ranks([flop], device=dev)[0]
     flop_max = shard.max_over_ranks([flop], device=dev)[0]
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": flop_all / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-            "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (smooth-field Q/K drawn on device, iid V; DESIGN.md §Inputs)",
-            "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d,
-                       "layers": args.layers, "mask": mode, "units_per_rank": hi - lo,
-                       "parallelism": f"(batch,head)-sharded x{ws}; NCCL gather of the last "
-                       "layer's O to rank 0 inside the step",
-                       "l2": "inputs larger than L2, no flush"},
-            "ms_per_layer": ms / args.layers, "clocks": clocks,
-            "rank_imbalance_active_flop": flop_max / (flop_all / ws),
-            "gpu_launches": 5 * args.layers * args.steps}), flush=True)
+    ms_min = -shard.max_over_ranks([-ms_local], device=dev)[0]
+    o_bytes_to_rank0 = (units - (shard.unit_range(ws, 0, units)[1])) * w.N * w.d * 2
+    res = {
+        "value": flop_all / (ms * 1e-3) / 1e12, "ms_per_step": ms,
+        "ms_per_layer": ms / args.layers, "gather_ms": gather_ms if ws > 1 else 0.0,
+        "gather_bytes_to_rank0": o_bytes_to_rank0 if ws > 1 else 0,
+        "gather_gbs": (o_bytes_to_rank0 / (gather_ms * 1e-3) / 1e9) if ws > 1 and gather_ms > 0
+        else None,
+        "rank_imbalance_active_flop": flop_max / (flop_all / ws),
+        "rank_time_spread": ms / ms_min if ms_min > 0 else None,
+        "units_per_rank": hi - lo, "layers": args.layers, "mask": mode,
+        "active_tflop_per_step": flop_all / 1e12,
+    }
+    if sub or rank != 0:
+        return res
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": "TFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (smooth-field Q/K drawn on device per global unit, iid V; "
+                "DESIGN.md §Inputs)",
+        "config": {"workload": w.name, "B": w.B, "H": w.H, "N": w.N, "d": w.d,
+                   "layers": args.layers, "mask": mode, "units_per_rank": hi - lo,
+                   "parallelism": f"(batch,head)-sharded x{ws}; NCCL gather of the last "
+                   "layer's O to rank 0 inside the step",
+                   "backend": "gloo (shared GPU, testing)" if _SHARE_GPU else "nccl",
+                   "l2": "inputs larger than L2, no flush"},
+        "ms_per_layer": res["ms_per_layer"], "gather_ms": res["gather_ms"],
+        "gather_bytes_to_rank0": res["gather_bytes_to_rank0"], "gather_gbs": res["gather_gbs"],
+        "rank_imbalance_active_flop": res["rank_imbalance_active_flop"],
+        "rank_time_spread": res["rank_time_spread"], "clocks": clocks,
+        "e2e": None,
+        "gpu_launches": (5 + int(mp["keep_min"] < mp["keep_max"])) * args.layers * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return res
 
 
-def main():
-    args = parse()
-    ws, rank, local = dist_env()
-    if args.impl == "reference":
-        run_reference(args, ws, rank)
-        return
-    if args.workload == "wan_stack":
-        dev = bind_device(local)
-        if ws > 1:
-            init_dist(dev)
-        run_stack(args, ws, rank, local, dev)
-        if ws > 1:
-            torch.distributed.destroy_process_group()
-        return
-    dev = bind_device(local)
-    if ws > 1:
-        init_dist(dev)
+def measure_layer(args, workload: str, dev, local: int, *, headline: bool):
+    """One attention layer (BJ configs[1] / configs[2]) on one GPU."""
     from paper_2508_10774_b200 import asa as A
 
-    w = inputs.WORKLOADS[args.workload]
-    # weak scaling: one sample (H units) per rank; rank r = sample r, units [rH, rH + H)
+    w = inputs.WORKLOADS[workload]
     q_h, k_h, v_h = inputs.smooth(1, w.H, w.N, w.d, w.grid, w.n_text, w.ell, w.beta, w.sigma_n,
-                                  seed=42 + rank)
+                                  seed=42)
     BH, N, d = q_h.shape
     Nb = (N + 127) // 128
-    mp, mode = mask_params(w, args, Nb)
+    mp, mode = mask_params(args, workload, Nb)
     impl = {"auto": A.ATTN_AUTO, "tcgen05": A.ATTN_TCGEN05, "mma": A.ATTN_MMA_SYNC,
             "pair": A.ATTN_TCGEN05_PAIR, "triple": A.ATTN_TCGEN05_TRIPLE}[args.attn]
     q, k, v = (t.to(dev) for t in (q_h, k_h, v_h))
     stream = torch.cuda.current_stream()
-    unit_offset = rank * w.H
-
-    gt = args.variant == "asa_gt"
+    gt = args.variant == "asa_gt" and headline
+    ev_mid = [_ev()]
 
     def step():
         if gt:  # ASA_GT (P:135): MeanPool_n counts as mask-side work
             kg, vg = A.blade_gt_pool(k, v, window=args.window)
-        m = A.blade_asa_mask(q, k, unit_offset=unit_offset, want_mask=False, **mp)
-        ev_mid.record(stream)
+        m = A.blade_asa_mask(q, k, want_mask=False, **mp)
+        ev_mid[0].record(stream)
         if gt:
             A.blade_bsa_gt_fwd(q, k, v, m.kv_idx, m.kv_cnt, kg, vg, window=args.window,
                                impl=impl)
@@ -380,7 +444,6 @@ def main():
             A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl)
         return m
 
-    ev_mid = torch.cuda.Event(enable_timing=True)
     for _ in range(max(args.warmup, 3)):
         m = step()
     torch.cuda.synchronize()
@@ -391,68 +454,45 @@ def main():
     refined = int(m.n_refined.item())
     sparsity = 1.0 - kv_cnt_np.sum() / (BH * Nb * Nb)
 
-    # timed region: per-step events for the attention share
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if ws > 1:
-        torch.distributed.barrier()
+    fo = [None]
+
+    def fused():
+        if gt:
+            fo[0] = A.blade_asa_gt_fwd(q, k, v, window=args.window, impl=impl, out=fo[0], **mp)
+        else:
+            fo[0] = A.blade_asa_fwd(q, k, v, impl=impl, out=fo[0], **mp)
+
+    for _ in range(3):
+        fused()
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    time.sleep(0.3)
-    t_begin = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_begin.record(stream)
+    clk = ClockSampler(local) if headline else None
+    time.sleep(0.3 if headline else 0.0)
+    # (1) the production single call: the headline
+    fused_ms = time_loop(fused, args.steps, stream)
+    # (2) the same K steps as two calls, with an event between them
+    starts = [_ev() for _ in range(args.steps)]
+    mids = [_ev() for _ in range(args.steps)]
+    ends = [_ev() for _ in range(args.steps)]
     for s in range(args.steps):
         starts[s].record(stream)
-        ev_mid = mids[s]
+        ev_mid[0] = mids[s]
         step()
         ends[s].record(stream)
-    t_end.record(stream)
     torch.cuda.synchronize()
-    total_ms = t_begin.elapsed_time(t_end)
+    clocks = clk.stop() if clk else None
+    two_ms = statistics.mean(starts[s].elapsed_time(ends[s]) for s in range(args.steps))
     attn_ms = statistics.mean(mids[s].elapsed_time(ends[s]) for s in range(args.steps))
     mask_ms = statistics.mean(starts[s].elapsed_time(mids[s]) for s in range(args.steps))
-    from paper_2508_10774_b200 import shard
-    total_ms, attn_ms, mask_ms = shard.max_over_ranks([total_ms, attn_ms, mask_ms], device=dev)
-    flop_all = shard.sum_over_ranks([flop], device=dev)[0]
-    flop_max = shard.max_over_ranks([flop], device=dev)[0]
-    ms_per_step = total_ms / args.steps
-    value = flop_all / (ms_per_step * 1e-3) / 1e12
-
-    # the production single call (blade_asa_fwd: the attention launched as a
-    # programmatic dependent of the mask's last kernel), same inputs
-    # (ASA_GT: blade_asa_gt_fwd, MeanPool_n + mask + attention in one call)
-    fused_ms = None
-    if not (gt and impl == A.ATTN_MMA_SYNC):
-        def fused(out=None):
-            if gt:
-                return A.blade_asa_gt_fwd(q, k, v, window=args.window, unit_offset=unit_offset,
-                                          impl=impl, out=out, **mp)
-            return A.blade_asa_fwd(q, k, v, unit_offset=unit_offset, impl=impl, out=out, **mp)
-
-        fo = fused()
-        for _ in range(3):
-            fused(fo)
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            fused(fo)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        fused_ms = shard.max_over_ranks([f0.elapsed_time(f1) / args.steps], device=dev)[0]
-
-    clocks = clk.stop()  # sampled over both timed loops
-    # headline = the production single call when available (same work, same
-    # inputs); the two-call loop above gives the mask / attention split
-    ms_two_calls = ms_per_step
-    if fused_ms is not None:
-        ms_per_step = fused_ms
-        value = flop_all / (ms_per_step * 1e-3) / 1e12
-
+    pk, pk_src = peaks()
+    attn_tflops = flop / (attn_ms * 1e-3) / 1e12
+    res = {"workload": w.name, "value": flop / (fused_ms * 1e-3) / 1e12,
+           "ms_per_step": fused_ms, "ms_mask": mask_ms, "ms_attn": attn_ms,
+           "ms_per_step_two_calls": two_ms, "sparsity": round(float(sparsity), 4),
+           "rows_refined_fp64": refined, "mask": mode, "keep": [mp["keep_min"], mp["keep_max"]],
+           "attn_tflops": attn_tflops, "attn_frac": attn_tflops / pk["bf16_tflops"],
+           "active_tflop": flop / 1e12, "steps": args.steps}
+    if not headline:
+        return res
     # e2e: host buffers through the ABI, copies inside the timed region
     e2e = None
     if not args.no_e2e and not gt:  # the host-buffer entry point runs plain ASA
@@ -462,34 +502,23 @@ def main():
 
         def e2e_step():
             # the public host-buffer entry point: chunked H2D / compute / D2H overlap
-            A.blade_asa_fwd_host(qp, kp, vp, unit_offset=unit_offset, impl=impl,
-                                 chunk_units=args.e2e_chunk, o=o_host, lse=lse_host, **mp)
+            A.blade_asa_fwd_host(qp, kp, vp, impl=impl, chunk_units=args.e2e_chunk, o=o_host,
+                                 lse=lse_host, **mp)
 
         for _ in range(2):
             e2e_step()
-        if ws > 1:
-            torch.distributed.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = shard.max_over_ranks([e0.elapsed_time(e1) / args.steps], device=dev)[0]
-        e2e = {"value": flop_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        e2e_ms = time_loop(e2e_step, args.steps, stream)
+        e2e = {"value": flop / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e2e_ms, "api": "blade_asa_fwd_host (C ABI, pinned host buffers, "
                "chunked copy/compute overlap)", "h2d_bytes_per_step": 3 * q_h.numel() * 2,
                "d2h_bytes_per_step": q_h.numel() * 2 + BH * N * 4}
-
-    pk, pk_src = peaks()
-    attn_tflops = flop / (attn_ms * 1e-3) / 1e12
-    roof = {"kernel": "blade_bsa_fwd (attention)", "bound": "tensor", "achieved": attn_tflops,
-            "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": attn_tflops / pk["bf16_tflops"],
+    roof = {"kernel": "attn_tc2_kernel (blade_bsa_fwd)", "bound": "tensor",
+            "achieved": attn_tflops, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": attn_tflops / pk["bf16_tflops"],
             "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)",
-            "traffic": traffic_for(args.workload, "attn"),
-            "attn_ms": attn_ms, "mask_ms": mask_ms,
-            "attn_share": attn_ms / (attn_ms + mask_ms)}
+            "traffic": traffic_for(args.workload or "wan", "attn"),
+            "attn_ms": attn_ms, "mask_ms": mask_ms, "attn_share": attn_ms / (attn_ms + mask_ms)}
     # the mask side: the sampled probe is exponential- (MUFU-)
     # and tensor-bound, the gather / list writes HBM-bound; all three rates
     # over the whole blade_asa_mask time (sample, probe, select, refine)
@@ -506,53 +535,91 @@ def main():
                  / pk["bf16_tflops"],
                  "hbm_gbs_algorithmic": mask_bytes / (mask_ms * 1e-3) / 1e9,
                  "hbm_frac": mask_bytes / (mask_ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    res.update(e2e=e2e, roofline=roof, mask_roofline=mask_roof, clocks=clocks,
+               flop=flop, BH=BH, N=N, d=d, mp=mp, q_h=q_h, k_h=k_h, v_h=v_h, gt=gt,
+               sustained=None)
+    # sustained: the headline call back to back for ~args.sustained_s seconds
+    if not args.no_extra and args.sustained_s > 0:
+        n = max(args.steps, int(args.sustained_s / (fused_ms * 1e-3)))
+        clk2 = ClockSampler(local)
+        s_ms = time_loop(fused, n, stream)
+        res["sustained"] = {"steps": n, "ms_per_step": s_ms,
+                            "value": flop / (s_ms * 1e-3) / 1e12, "clocks": clk2.stop(),
+                            "peak_for_context": pk.get("bf16_tflops_sustained")}
+    return res
 
+
+def run_single(args, dev, local):
+    from paper_2508_10774_b200 import asa as A  # noqa: F401 (fails loudly without the .so)
+    workload = args.workload or "wan"
+    r = measure_layer(args, workload, dev, local, headline=True)
+    extra = {}
+    if not args.no_extra and workload == "wan" and not args.tau_mode and args.keep is None:
+        extra["cog"] = measure_layer(args, "cog", dev, local, headline=False)
+        torch.cuda.empty_cache()
+        sub_args = argparse.Namespace(**{**vars(args), "steps": min(args.steps, 10),
+                                         "warmup": 3})
+        extra["stack_1gpu"] = run_stack(sub_args, 1, 0, local, dev, sub=True)
+        torch.cuda.empty_cache()
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        f1, sec, desc = oracle_sample(q_h, k_h, v_h, w, mp, 2, None)
+    if not args.no_cpu:
+        f1, sec, desc, _, _ = oracle_sample(r["q_h"], r["k_h"], r["v_h"], r["N"], r["d"],
+                                            r["mp"], 2, None)
         cpu = {"value": f1 / sec / 1e12, "unit": "TFLOP/s", "cores": cores_used(),
                "kind": "oracle", "sample": desc}
+    gt = r["gt"]
+    mp = r["mp"]
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": "TFLOP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (smooth-field Q/K, iid V; DESIGN.md §Inputs)",
+        "config": {"workload": r["workload"], "B": 1, "H": r["BH"], "N": r["N"], "d": r["d"],
+                   "variant": args.variant + (f" (window {args.window})" if gt else ""),
+                   "mask": r["mask"], "tau": mp["tau"], "keep": r["keep"],
+                   "block": 128, "samples": 16, "sparsity": r["sparsity"],
+                   "parallelism": "single GPU (the N>1 lines: configs[4] strong scaling)",
+                   "attn_impl": args.attn, "l2": "inputs larger than L2 (Q+K+V "
+                   f"{3 * r['q_h'].numel() * 2 / 1e6:.0f} MB per step), no flush",
+                   "rows_refined_fp64": r["rows_refined_fp64"],
+                   "probe_gflop": probe_flop(r["BH"], r["N"], r["d"]) / 1e9},
+        "ms_mask": r["ms_mask"], "ms_attn": r["ms_attn"],
+        "ms_per_step_two_calls": r["ms_per_step_two_calls"],
+        "step_api": ("blade_asa_gt_fwd" if gt else "blade_asa_fwd") +
+                    " (one call; attention a programmatic dependent of the mask's last kernel)",
+        "clocks": r["clocks"], "e2e": r["e2e"], "roofline": r["roofline"],
+        "mask_roofline": r["mask_roofline"], "cpu_baseline": cpu,
+        "sustained": r["sustained"],
+        "gpu_launches": (5 + int(gt) + int(mp["keep_min"] < mp["keep_max"])) * args.steps,
+    }
+    for key, val in extra.items():
+        line[key] = val
+    print(json.dumps(line), flush=True)
 
-    gather = None
-    if args.gather and ws > 1:
-        o_local, _ = A.blade_bsa_fwd(q, k, v, m.kv_idx, m.kv_cnt, impl=impl)
-        torch.cuda.synchronize()
-        g0 = time.perf_counter()
-        o_all = shard.gather_units(o_local, ws * w.H)
-        torch.cuda.synchronize()
-        gather = {"bytes_to_rank0": (ws - 1) * o_local.numel() * 2,
-                  "seconds_wallclock": time.perf_counter() - g0,
-                  "shape": list(o_all.shape) if o_all is not None else None}
-    launches_per_step = 5 + int(gt)  # [gt_pool], sample_gather, probe, select, refine, attention
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (smooth-field Q/K, iid V; DESIGN.md §Inputs)",
-            "config": {"workload": w.name, "B_total": ws, "H": w.H, "N": N, "d": d,
-                       "variant": args.variant + (f" (window {args.window})" if gt else ""),
-                       "mask": mode, "tau": mp["tau"], "keep": [mp["keep_min"], mp["keep_max"]],
-                       "block": 128, "samples": 16, "sparsity": round(float(sparsity), 4),
-                       "parallelism": f"(batch,head)-sharded x{ws}, no collective",
-                       "attn_impl": args.attn, "l2": "inputs larger than L2 (Q+K+V "
-                       f"{3 * q_h.numel() * 2 / 1e6:.0f} MB per rank per step), no flush",
-                       "rows_refined_fp64": refined,
-                       "probe_gflop": probe_flop(BH, N, d) / 1e9},
-            "ms_mask": mask_ms, "ms_attn": attn_ms, "ms_per_step_two_calls": ms_two_calls,
-            "step_api": (("blade_asa_gt_fwd" if gt else "blade_asa_fwd") +
-                         " (one call; attention a programmatic dependent of the mask's last "
-                         "kernel)" if fused_ms is not None else
-                         "blade_asa_mask + blade_bsa_fwd"),
-            "clocks": clocks, "e2e": e2e, "roofline": roof, "mask_roofline": mask_roof,
-            "cpu_baseline": cpu,
-            "gpu_launches": launches_per_step * args.steps,
-            "rank_imbalance_active_flop": flop_max / (flop_all / ws),
-            "gather": gather,
-        }
-        print(json.dumps(line), flush=True)
+
+def main():
+    args = parse()
+    in_torchrun = "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not in_torchrun:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    ws, rank, local = dist_env()
+    if in_torchrun and ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        sys.exit(2)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    dev = bind_device(local)
     if ws > 1:
-        torch.distributed.destroy_process_group()
+        init_dist(dev)
+    try:
+        if ws > 1 or args.workload == "wan_stack":
+            run_stack(args, ws, rank, local, dev)
+        else:
+            run_single(args, dev, local)
+    finally:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -226,11 +226,13 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
           tc::mma_ts(tmem + C::kColDQ, tmem + kColDS + ks * 8,
                      tc::sw128_desc(kb + ks * 2048, C::kPanel, 1024), idQ,
                      (n > 0 || ks > 0) ? 1 : 0);
-        tc::commit(bar_dq);
+        // only the last dQ MMA is awaited (tcgen05 ops of one thread complete
+        // in order): one commit, one phase, every phase has a waiter
+        if (n + 1 == total) tc::commit(bar_dq);
         tc::commit(bar_kempty + (n % C::kRingK));
         if (n + 1 < total) issue_dP(n + 1);
       }
-      tc::mbar_wait(bar_dq, (total - 1) & 1);
+      tc::mbar_wait(bar_dq, 0);
     }
   } else if (warp < kEW) {
     // ===================== elementwise: P, dS =====================
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     }
     // epilogue: dQ * scale -> bf16
     if (total > 0) {
-      tc::mbar_wait(bar_dq, (total - 1) & 1);
+      tc::mbar_wait(bar_dq, 0);
       tc::fence_after_sync();
     }
     __nv_bfloat16* out = dQ + (u * N + row) * int64_t(D);
@@ -493,14 +495,14 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
         tc::mbar_wait(bar_ds, n & 1);
         tc::fence_after_sync();
         ts(C::kColDK, kColDSt, slot_q(n), n > 0);  // dK += dS^T Q_i
-        tc::commit(bar_dk);
+        if (n + 1 == cnt) tc::commit(bar_dk);  // only the last is awaited (see bar_dq)
         tc::commit(bar_empty + (n % C::kRing));
         if (n + 1 < cnt) {
           ss(C::kColDP, va, slot_q(n + 1) + C::kTile);  // dP^T(n+1) (after dK(n) read dS^T(n))
           tc::commit(bar_dp);
         }
       }
-      tc::mbar_wait(bar_dk, (cnt - 1) & 1);
+      tc::mbar_wait(bar_dk, 0);
     }
   } else if (warp < kEW) {
     // ===================== elementwise: P^T, dS^T (thread = key row) ========
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     }
     // epilogue: dK * scale, dV -> bf16 (key rows; zero if no query keeps j)
     if (cnt > 0) {
-      tc::mbar_wait(bar_dk, (cnt - 1) & 1);
+      tc::mbar_wait(bar_dk, 0);
       tc::fence_after_sync();
     }
     const int krow = j * 128 + r;

@@ -314,7 +314,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
           tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
                      tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                      (k > 0 || ks > 0) ? 1 : 0);
-        tc::commit(bar_pv + t);
+        // bar_pv: with kSepP the softmax waits for every P V; otherwise only
+        // the last one is awaited (S(n) is issued after P V(n-1), and tcgen05
+        // ops of one thread complete in order), so only the last is committed
+        // and every phase of the barrier has a waiter (compute-sanitizer
+        // synccheck flags a phase nobody waits for)
+        if (C::kSepP || k + 1 == (t ? cnt1 : cnt0)) tc::commit(bar_pv + t);
         tc::commit(bar_vempty + s);
         ++gv;
       };
@@ -404,8 +409,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
       }
       }  // !kHalfS
       // drain: the last commits must land before the CTA's smem is released
-      if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, (cnt0 - 1) & 1);
-      if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, (cnt1 - 1) & 1);
+      constexpr bool kPvEvery = C::kSepP || C::kHalfS;  // one bar_pv phase per item
+      if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, kPvEvery ? (cnt0 - 1) & 1 : 0);
+      if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, kPvEvery ? (cnt1 - 1) & 1 : 0);
     }
   }
   } else {
@@ -664,7 +670,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
     if (cnt > 0) {
       // epilogue: O / l -> bf16, LSE
-      tc::mbar_wait(bar_pv + t, (cnt - 1) & 1);
+      tc::mbar_wait(bar_pv + t, (C::kSepP || C::kHalfS) ? (cnt - 1) & 1 : 0);
       tc::fence_after_sync();
       const int row = (i0 + t) * 128 + r;
       const float inv = 1.f / l_sum;

@@ -134,26 +134,39 @@ def make(workload: str | Workload, recipe: str = "smooth", seed: int = 42,
     raise ValueError(recipe)
 
 
-def smooth_device(units: int, N: int, d: int, grid: tuple, device, n_text: int = 0,
+def unit_seed(base: int, u_global: int) -> int:
+    """Seed of one (batch, head) unit: a function of the GLOBAL unit index
+    only, so every sharding of a batch draws identical tensors per unit."""
+    return (base * 1_000_003 + u_global) & ((1 << 63) - 1)
+
+
+def smooth_device(units, N: int, d: int, grid: tuple, device, n_text: int = 0,
                   ell: float = 3.0, beta: float = 9.0, sigma_n: float = 0.1, seed: int = 42):
     """The ``smooth`` recipe drawn with torch's CUDA generator directly on the
     device (same distribution, different stream of random numbers than the
     numpy version), for workloads too large to generate on the host (the
-    30-layer batch-8 stack, BASELINE.json configs[4]).  Returns bf16
-    [units, N, d] q, k, v on ``device``."""
+    30-layer batch-8 stack, BASELINE.json configs[4]).  ``units`` is the range
+    (or list) of GLOBAL unit indices to draw; unit u uses its own generator
+    seeded with ``unit_seed(seed, u)``, so a rank drawing units [lo, hi) gets
+    exactly the slice a single-GPU run draws.  Returns bf16 [len(units), N, d]
+    q, k, v on ``device``."""
+    if isinstance(units, int):
+        units = range(units)
+    units = list(units)
     g = torch.Generator(device=device)
-    g.manual_seed(seed)
     pos = torch.from_numpy(grid_positions(grid)).to(device)
-    q = torch.empty((units, N, d), dtype=torch.bfloat16, device=device)
+    q = torch.empty((len(units), N, d), dtype=torch.bfloat16, device=device)
     k = torch.empty_like(q)
-    for u in range(units):
+    v = torch.empty_like(q)
+    for n, u in enumerate(units):
+        g.manual_seed(unit_seed(seed, u))
         W = torch.randn((3, d), generator=g, device=device) / ell
         phi = torch.rand(d, generator=g, device=device) * (2 * np.pi)
         F = (2.0 / d) ** 0.5 * torch.cos(pos @ W + phi)
         if n_text:
             T = torch.randn((n_text, d), generator=g, device=device) / d ** 0.5
             F = torch.cat([T, F], 0)
-        q[u] = beta * F + sigma_n * torch.randn((N, d), generator=g, device=device)
-        k[u] = beta * F + sigma_n * torch.randn((N, d), generator=g, device=device)
-    v = torch.randn((units, N, d), generator=g, device=device).to(torch.bfloat16)
+        q[n] = beta * F + sigma_n * torch.randn((N, d), generator=g, device=device)
+        k[n] = beta * F + sigma_n * torch.randn((N, d), generator=g, device=device)
+        v[n] = torch.randn((N, d), generator=g, device=device)
     return q, k, v

@@ -33,9 +33,15 @@ def gather_units(local: torch.Tensor, units: int, group=None, dst: int = 0):
         raise ValueError(f"rank {rank}: expected {hi - lo} units, got {local.shape[0]}")
     biggest = max(unit_range(world, r, units)[1] - unit_range(world, r, units)[0]
                   for r in range(world))
-    pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype,
-                      device=local.device)
-    pad[:hi - lo] = local
+    # gloo has no CUDA gather: stage through host memory (testing on one GPU)
+    dev = local.device
+    if dist.get_backend(group) == "gloo" and local.is_cuda:
+        dev = torch.device("cpu")
+    if hi - lo == biggest and local.device == dev and local.is_contiguous():
+        pad = local  # even share: no staging copy
+    else:
+        pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
+        pad[:hi - lo] = local
     parts = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
     dist.gather(pad, parts, dst=dst, group=group)
     if rank != dst:
@@ -49,14 +55,21 @@ def gather_units(local: torch.Tensor, units: int, group=None, dst: int = 0):
 
 def max_over_ranks(values, device=None, group=None) -> list[float]:
     """Element-wise max of a list of floats over all ranks (for timings)."""
-    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    t = torch.tensor(list(values), dtype=torch.float64, device=_red_dev(device, group))
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.tolist()
 
 
 def sum_over_ranks(values, device=None, group=None) -> list[float]:
-    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    t = torch.tensor(list(values), dtype=torch.float64, device=_red_dev(device, group))
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t.tolist()
+
+
+def _red_dev(device, group):
+    """Reductions run where the backend can: gloo on the host."""
+    if dist.is_initialized() and dist.get_backend(group) == "gloo":
+        return torch.device("cpu")
+    return device
