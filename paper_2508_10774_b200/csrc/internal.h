@@ -27,7 +27,7 @@ struct MaskProblem {
 struct MaskWorkspace {
   size_t off_qs, off_ks, off_pimp, off_counters, off_flags, off_done, off_r64, off_mpart,
       off_lpart, total;
-  int nchunks;  // refine key chunks (64 sampled keys for k <= 64, else 128)
+  int nchunks;  // refine key chunks of 128 sampled keys
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -36,7 +36,7 @@ inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   MaskWorkspace w{};
   const size_t rows = size_t(p.BH) * p.Nb;            // (unit, q-block) rows
   const size_t nk = size_t(p.Nb) * p.kk;              // padded sampled rows / unit
-  const size_t ck = p.kk <= 64 ? 64 : 128;
+  const size_t ck = 128;  // sampled keys per refine work item (RF_CK)
   w.nchunks = int((nk + ck - 1) / ck);
   size_t o = 0;
   w.off_qs = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);

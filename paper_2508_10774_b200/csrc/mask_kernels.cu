@@ -33,6 +33,50 @@ namespace {
 
 constexpr int kMaxNb = 512;
 
+// Ascending bitonic sort of P = 32 E (hash, offset) pairs across a warp, E
+// per lane at positions x = E lane + e (distances < E in registers, larger
+// ones by shuffles); ties of the hash broken by the offset (reading R-1).
+template <int E>
+BLADE_DEVINL void bitonic_pairs(uint64_t (&r)[E], int (&o)[E], int lane) {
+  auto less = [](uint64_t ra, int oa, uint64_t rb, int ob) {
+    return ra < rb || (ra == rb && oa < ob);
+  };
+#pragma unroll
+  for (int kb = 2; kb <= 32 * E; kb <<= 1) {
+#pragma unroll
+    for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+      if (jb < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int pe = e ^ jb;
+          if (pe > e) {
+            const bool up = ((lane * E + e) & kb) == 0;
+            const bool sw = up ? less(r[pe], o[pe], r[e], o[e]) : less(r[e], o[e], r[pe], o[pe]);
+            if (sw) {
+              const uint64_t tr = r[e]; r[e] = r[pe]; r[pe] = tr;
+              const int to = o[e]; o[e] = o[pe]; o[pe] = to;
+            }
+          }
+        }
+      } else {
+        const int lm = jb / E;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t orr = __shfl_xor_sync(0xffffffffu, r[e], lm);
+          const int oo = __shfl_xor_sync(0xffffffffu, o[e], lm);
+          const bool up = ((lane * E + e) & kb) == 0;
+          const bool mine_first = less(r[e], o[e], orr, oo);
+          if (mine_first != (lower == up)) {
+            r[e] = orr;
+            o[e] = oo;
+          }
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K-mask.1  sampling + gather
 // ---------------------------------------------------------------------------
@@ -64,71 +108,82 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
     const int wh = share_qk ? 0 : which;
     const uint64_t key =
         smix(smix(smix(seed, uint64_t(unit_offset + u)), uint64_t(i)), uint64_t(wh));
-    // bitonic sort of the 128 (hash, offset) pairs, ascending; 4 per lane at
-    // positions x = 4*lane + e; invalid offsets carry the maximal hash and
-    // their (larger) offset, so they sort after every valid one
-    uint64_t r[4];
-    int o[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      o[e] = lane * 4 + e;
-      r[e] = o[e] < valid ? smix(key, uint64_t(o[e])) : ~0ull;
-    }
-    auto less = [](uint64_t ra, int oa, uint64_t rb, int ob) {
-      return ra < rb || (ra == rb && oa < ob);
-    };
-#pragma unroll
-    for (int kb = 2; kb <= 128; kb <<= 1) {
-#pragma unroll
-      for (int jb = kb >> 1; jb > 0; jb >>= 1) {
-        if (jb < 4) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int pe = e ^ jb;
-            if (pe > e) {
-              const bool up = ((lane * 4 + e) & kb) == 0;
-              const bool sw = up ? less(r[pe], o[pe], r[e], o[e]) : less(r[e], o[e], r[pe], o[pe]);
-              if (sw) {
-                const uint64_t tr = r[e]; r[e] = r[pe]; r[pe] = tr;
-                const int to = o[e]; o[e] = o[pe]; o[pe] = to;
-              }
-            }
-          }
-        } else {
-          const int lm = jb >> 2;
-          const bool lower = (lane & lm) == 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint64_t orr = __shfl_xor_sync(0xffffffffu, r[e], lm);
-            const int oo = __shfl_xor_sync(0xffffffffu, o[e], lm);
-            const bool up = ((lane * 4 + e) & kb) == 0;
-            const bool mine_first = less(r[e], o[e], orr, oo);
-            if (mine_first != (lower == up)) {
-              r[e] = orr;
-              o[e] = oo;
-            }
-          }
-        }
-      }
-    }
-    // the k_i smallest sit at positions 0..k_i-1; emit their offsets ascending
     __shared__ uint32_t sel_bits[8][4];
+    __shared__ uint64_t cand_h[8][64];
+    __shared__ int cand_o[8][64];
     if (lane < 4) sel_bits[warp][lane] = 0u;
-    __syncwarp();
+    // Fast path (k_i <= 16): only offsets whose hash lies below a threshold
+    // T can be among the k_i smallest when at least k_i hashes do; with
+    // T / 2^64 = 40 / valid about 40 candidates survive (>= 16 and <= 64
+    // except with probability ~1e-5), which are sorted 2 per lane instead of
+    // all 128.  Exact: the k_i smallest (hash, offset) pairs of all offsets are
+    // the k_i smallest of the candidates whenever there are >= k_i of them;
+    // otherwise (or > 64) the full 128-pair sort below runs.
+    bool fast = false;
+    if (ki <= 16) {
+      const uint64_t T = valid <= 40 ? ~0ull
+                                     : uint64_t(40.0 / double(valid) * 18446744073709551616.0);
+      uint64_t h[4];
+      int cnt = 0, pos[4];
+      bool c[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (lane * 4 + e < ki) atomicOr(&sel_bits[warp][o[e] >> 5], 1u << (o[e] & 31));
-    __syncwarp();
-    if (lane == 0) {
-      int pos = 0;
-      for (int w = 0; w < 4; ++w) {
-        uint32_t bits = sel_bits[warp][w];
-        while (bits) {
-          const int bb = __ffs(bits) - 1;
-          bits &= bits - 1;
-          offs[warp][pos++] = w * 32 + bb;
-        }
+      for (int e = 0; e < 4; ++e) {
+        const int o = lane + 32 * e;
+        h[e] = o < valid ? smix(key, uint64_t(o)) : ~0ull;
+        c[e] = o < valid && h[e] <= T;
+        const uint32_t bal = __ballot_sync(0xffffffffu, c[e]);
+        pos[e] = cnt + __popc(bal & ((1u << lane) - 1u));
+        cnt += __popc(bal);
       }
+      if (cnt >= ki && cnt <= 64) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c[e]) {
+            cand_h[warp][pos[e]] = h[e];
+            cand_o[warp][pos[e]] = lane + 32 * e;
+          }
+        __syncwarp();
+        uint64_t r[2];
+        int o[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int x = lane * 2 + e;
+          r[e] = x < cnt ? cand_h[warp][x] : ~0ull;
+          o[e] = x < cnt ? cand_o[warp][x] : 1024 + x;  // pads sort last
+        }
+        bitonic_pairs<2>(r, o, lane);
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (lane * 2 + e < ki) atomicOr(&sel_bits[warp][o[e] >> 5], 1u << (o[e] & 31));
+        fast = true;
+      }
+    }
+    if (!fast) {
+      // bitonic sort of the 128 (hash, offset) pairs, ascending; 4 per lane at
+      // positions x = 4*lane + e; invalid offsets carry the maximal hash and
+      // their (larger) offset, so they sort after every valid one
+      uint64_t r[4];
+      int o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        o[e] = lane * 4 + e;
+        r[e] = o[e] < valid ? smix(key, uint64_t(o[e])) : ~0ull;
+      }
+      bitonic_pairs<4>(r, o, lane);
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (lane * 4 + e < ki) atomicOr(&sel_bits[warp][o[e] >> 5], 1u << (o[e] & 31));
+    }
+    // the k_i selected offsets, ascending: per 32-offset word, each lane
+    // places its offset at the word's running count
+    __syncwarp();
+    int base = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t bits = sel_bits[warp][w];
+      if ((bits >> lane) & 1u) offs[warp][base + __popc(bits & ((1u << lane) - 1u))] = w * 32 + lane;
+      base += __popc(bits);
     }
   }
   __syncwarp();
@@ -466,9 +521,33 @@ __device__ void refine_select_cta(double* p, double* sorted, int* rank, double* 
   if (tid == 0) *kv_cnt_out = m;
 }
 
-// CK = sampled keys per work item (64 for k <= 64, 128 for k = 128): a thread
-// owns one key and RPT = 16 CK / 128 of the block's (up to 16) query rows.
-template <int D, int CK>
+// K-mask.4 on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64).  One CTA
+// (4 warps) per (queued row, chunk of 128 sampled keys), persistent grid.
+// The chunk's 128 key rows (bf16) are staged in shared memory once; warp w
+// owns keys [32 w, 32 w + 32) of the chunk (four n-tiles of 8) against 16 of
+// the block's sampled query rows at a time (two m-tiles of 8).  The d axis is
+// permuted so that lane l of a fragment walks d = (l & 3) (D/4) + kappa,
+// kappa = 0 .. D/4 - 1: every lane's operands for all D/4 k-steps are one
+// contiguous run of its row (four 16-byte loads per row), converted to fp64
+// on the fly (exact).  The sum over d is the same dot product as the oracle's
+// up to fp64 rounding order.  The accumulators give the chunk's exact-product
+// fp64 logits; per chunk the CTA leaves R (per key block), the chunk max M_c
+// and l_c = sum exp(L - M_c).  The CTA that finishes a row's last chunk
+// combines them (Alg. 3 l.14: M = max M_c, l = sum l_c e^{M_c - M}), forms
+// the fp64 P_imp row (l.17-19) and reselects it.  The reselection works on
+// the fp64 values (refine_select_cta).
+constexpr int RF_CK = 128;  // sampled keys per work item
+
+BLADE_DEVINL void dmma_m8n8k4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+BLADE_DEVINL double bf16_lo_f64(uint32_t w) { return double(__uint_as_float(w << 16)); }
+BLADE_DEVINL double bf16_hi_f64(uint32_t w) { return double(__uint_as_float(w & 0xffff0000u)); }
+
+template <int D>
 __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N, int Nb,
     int b, int kk, double scale, int nchunks, double tau, int lo, int hi,
@@ -476,22 +555,26 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     double* __restrict__ r64, double* __restrict__ mpart, double* __restrict__ lpart,
     float* __restrict__ pimp_out, uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx,
     int32_t* __restrict__ kv_cnt, int32_t* __restrict__ n_refined) {
-  constexpr int RPT = 16 * CK / RF_THREADS;  // query rows per thread
-  constexpr int NG = CK / 16;                // 16-key groups per item
-  constexpr int WPH = CK / 32;               // warps per row-half
-  __shared__ __align__(16) double sq[D][16];   // [d][s]: one LDS.128 serves two query rows
-  __shared__ double sRg[8][16];                // [16-key group][s] group max
-  __shared__ double sW[4][16];                 // per-warp partials
+  constexpr int RS = D * 2 + 16;   // smem row stride (bytes): conflict-free 16-byte reads
+  constexpr int DQ = D / 4;        // k-steps; each lane's contiguous d run
+  constexpr int NV = DQ / 8;       // 16-byte vectors per lane and row
+  // the staged key rows; the last CTA of a row reuses the space for the
+  // combine (P_imp row, sorted row, ranks) once every warp is past the MMA
+  __shared__ __align__(16) char sK[RF_CK * RS];
+  static_assert(RF_CK * RS >= kMaxNb * (8 + 8 + 4), "combine scratch must fit in sK");
+  double* sRow = reinterpret_cast<double*>(sK);    // refined P_imp row, then p~ (l.7)
+  double* sSorted = sRow + kMaxNb;                 // p~ in selection order (l.8)
+  int* sRank = reinterpret_cast<int*>(sSorted + kMaxNb);
+  __shared__ __align__(16) char sQ[16 * RS];
+  __shared__ double sRg[8][16];    // [16-key group][s] group max / combine scratch
+  __shared__ double sW[4][16];     // per-warp partials
   __shared__ double sMc[16];
-  __shared__ double sRow[kMaxNb];     // refined P_imp row, then p~ (l.7)
-  __shared__ double sSorted[kMaxNb];  // p~ in selection order (l.8)
-  __shared__ int sRank[kMaxNb];
   __shared__ double sMs[128];
   __shared__ double sScan[RF_THREADS];
   __shared__ int sCnt[RF_THREADS];
   __shared__ int last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kt = tid % CK, hr = tid / CK;
+  const int g8 = lane >> 2, kl = lane & 3;
   // a programmatically dependent attention launch (blade_asa_fwd) may start
   // now: its CTAs of refined rows wait in griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -511,56 +594,98 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     const int64_t u = row / Nb;
     const int i = int(row % Nb);
     const int ki = min(kk, min(b, N - i * b));
-    const int key = c * CK + kt;
-    const int jb = key / kk, rr = key - jb * kk;
-    const bool kvalid = key < NK && rr < min(kk, min(b, N - jb * b));
-    const __nv_bfloat16* kp = ks + (u * NK + min(key, NK - 1)) * int64_t(D);
+    __syncthreads();  // the previous item's smem reads are done
+    // stage the chunk's key rows (zero past N_k)
+    for (int e = tid; e < RF_CK * (D / 8); e += RF_THREADS) {
+      const int t = e / (D / 8), v8 = e % (D / 8);
+      const int key = c * RF_CK + t;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (key < NK) val = *reinterpret_cast<const uint4*>(ks + (u * NK + key) * int64_t(D) + v8 * 8);
+      *reinterpret_cast<uint4*>(sK + t * RS + v8 * 16) = val;
+    }
+    __syncthreads();
+    // validity of this lane's keys (2 per n-tile): padded samples of a ragged
+    // last block and slots past N_k get -inf
+    bool kv[4][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = c * RF_CK + warp * 32 + nt * 8 + 2 * kl + e;
+        const int jb = key / kk, rr = key - jb * kk;
+        kv[nt][e] = key < NK && rr < min(kk, min(b, N - jb * b));
+      }
     for (int sg = 0; sg < kk; sg += 16) {
       __syncthreads();
-      // coalesced: thread t reads 8 consecutive bf16 of query row t / (D/8)
       for (int e = tid; e < 16 * (D / 8); e += RF_THREADS) {
-        const int sq_s = e / (D / 8), d8 = (e % (D / 8)) * 8;
-        const uint4 raw = *reinterpret_cast<const uint4*>(
-            qs + (u * NK + int64_t(i) * kk + sg + sq_s) * D + d8);
-        const __nv_bfloat16* hq = reinterpret_cast<const __nv_bfloat16*>(&raw);
-#pragma unroll
-        for (int z = 0; z < 8; ++z) sq[d8 + z][sq_s] = double(__bfloat162float(hq[z]));
+        const int s = e / (D / 8), v8 = e % (D / 8);
+        const uint4 val = *reinterpret_cast<const uint4*>(
+            qs + (u * NK + int64_t(i) * kk + sg + s) * D + v8 * 8);
+        *reinterpret_cast<uint4*>(sQ + s * RS + v8 * 16) = val;
       }
       __syncthreads();
-      double L[RPT];
+      double acc[2][4][2];
 #pragma unroll
-      for (int q = 0; q < RPT; ++q) L[q] = 0.0;
-      uint4 krow[D / 8];  // the whole key row up front: one memory latency, not D/8
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int d0 = 0; d0 < D; d0 += 8) krow[d0 / 8] = *reinterpret_cast<const uint4*>(kp + d0);
+        for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+      // fragments: query row mt 8 + g8, key row 32 warp + 8 nt + g8, each lane
+      // walking its d run [kl DQ, kl DQ + DQ) one 16-byte vector at a time
+      const char* qrow = sQ + g8 * RS + kl * DQ * 2;
+      const char* krow = sK + (warp * 32 + g8) * RS + kl * DQ * 2;
+#pragma unroll 1
+      for (int v = 0; v < NV; ++v) {
+        uint4 qf[2], kf[4];
 #pragma unroll
-      for (int d0 = 0; d0 < D; d0 += 8) {
-        const uint4 raw = krow[d0 / 8];
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+        for (int mt = 0; mt < 2; ++mt)
+          qf[mt] = *reinterpret_cast<const uint4*>(qrow + mt * 8 * RS + v * 16);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const double kv = double(__bfloat162float(h[e]));
+        for (int nt = 0; nt < 4; ++nt)
+          kf[nt] = *reinterpret_cast<const uint4*>(krow + nt * 8 * RS + v * 16);
 #pragma unroll
-          for (int q = 0; q < RPT; q += 2) {
-            const double2 qq = *reinterpret_cast<const double2*>(&sq[d0 + e][hr * RPT + q]);
-            L[q] = fma(qq.x, kv, L[q]);
-            L[q + 1] = fma(qq.y, kv, L[q + 1]);
+        for (int w = 0; w < 4; ++w) {  // 32-bit word w of the vector: kappa 8v+2w, +1
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double a[2], bb[4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              const uint32_t x = reinterpret_cast<const uint32_t*>(&qf[mt])[w];
+              a[mt] = h ? bf16_hi_f64(x) : bf16_lo_f64(x);
+            }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const uint32_t x = reinterpret_cast<const uint32_t*>(&kf[nt])[w];
+              bb[nt] = h ? bf16_hi_f64(x) : bf16_lo_f64(x);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) dmma_m8n8k4(acc[mt][nt], a[mt], bb[nt]);
           }
         }
       }
+      // logits (Alg. 1 l.4: L = Q_s K_s^T * scale), -inf on invalid keys;
+      // per-(row, 16-key group) max: groups 2 warp + (nt >> 1)
 #pragma unroll
-      for (int q = 0; q < RPT; ++q) L[q] = kvalid ? L[q] * scale : -INFINITY;
-      // per 16-key group max (a key block when kk = 16); 16 consecutive lanes
+      for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
-      for (int q = 0; q < RPT; ++q) {
-        double v = L[q];
+        for (int gh = 0; gh < 2; ++gh) {
+          double v = -INFINITY;
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if ((lane & 15) == 0) sRg[kt >> 4][hr * RPT + q] = v;
+          for (int nt = 2 * gh; nt < 2 * gh + 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              acc[mt][nt][e] = kv[nt][e] ? acc[mt][nt][e] * scale : -INFINITY;
+              v = fmax(v, acc[mt][nt][e]);
+            }
+          v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 1));
+          v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 2));
+          if (kl == 0) sRg[warp * 2 + gh][mt * 8 + g8] = v;
+        }
       }
       __syncthreads();
-      const int gpb = kk / 16;     // 16-key groups per key block
-      const int nblk = CK / kk;    // key blocks per item (kk <= CK)
+      const int gpb = kk / 16;        // 16-key groups per key block
+      const int nblk = RF_CK / kk;    // key blocks per chunk (kk <= RF_CK)
       if (tid < 16 * nblk) {
         const int q = tid & 15, bl = tid >> 4;
         double v = -INFINITY;
@@ -571,24 +696,28 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
       if (tid < 16) {
         double v = -INFINITY;
 #pragma unroll
-        for (int gg = 0; gg < NG; ++gg) v = fmax(v, sRg[gg][tid]);
+        for (int gg = 0; gg < 8; ++gg) v = fmax(v, sRg[gg][tid]);
         sMc[tid] = v;
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < RPT; ++q) {
-        const double mc = sMc[hr * RPT + q];
-        double e = (L[q] == -INFINITY) ? 0.0 : exp(L[q] - mc);
+      for (int mt = 0; mt < 2; ++mt) {
+        const double mc = sMc[mt * 8 + g8];
+        double e = 0.0;
+        if (mc != -INFINITY) {
 #pragma unroll
-        for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if (lane == 0) sW[warp][q] = e;
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+              if (acc[mt][nt][x] != -INFINITY) e += exp(acc[mt][nt][x] - mc);
+        }
+        e += __shfl_xor_sync(0xffffffffu, e, 1);
+        e += __shfl_xor_sync(0xffffffffu, e, 2);
+        if (kl == 0) sW[warp][mt * 8 + g8] = e;
       }
       __syncthreads();
       if (tid < 16 && sg + tid < ki) {
-        const int h2 = tid / RPT, q = tid % RPT;  // the row-half that owns query row tid
-        double l = 0.0;
-#pragma unroll
-        for (int w = 0; w < WPH; ++w) l += sW[h2 * WPH + w][q];
+        const double l = sW[0][tid] + sW[1][tid] + sW[2][tid] + sW[3][tid];
         const int64_t o = (int64_t(f) * nchunks + c) * kk + sg + tid;
         mpart[o] = sMc[tid];
         lpart[o] = l;
@@ -752,14 +881,9 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     if (e != cudaSuccess) return e;
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
-  if (p.kk <= 64)
-    refine_kernel<D, 64><<<148 * 3, RF_THREADS, 0, stream>>>(
-        qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
-        flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
-  else
-    refine_kernel<D, 128><<<148 * 3, RF_THREADS, 0, stream>>>(
-        qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
-        flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
+  refine_kernel<D><<<148 * 3, RF_THREADS, 0, stream>>>(
+      qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
+      flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
 #ifdef BLADE_RF_TIMING
   {
     static int calls = 0;
