@@ -25,12 +25,23 @@ struct MaskProblem {
 
 // Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
 struct MaskWorkspace {
-  size_t off_qs, off_ks, off_pimp, off_counters, off_flags, off_done, off_r64, off_mpart,
-      off_lpart, total;
+  size_t off_srow, off_qs, off_ks, off_pimp, off_counters, off_flags, off_done, off_r64,
+      off_mpart, off_lpart, total;
   int nchunks;  // refine key chunks of 128 sampled keys
+  int nkpad;    // sampled slots per unit padded to whole 128-slot tiles
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// K-mask.2 on the probe2.cu tcgen05 probe (else probe_tc.cu / the mma.sync probe)?
+bool probe2_supported(int d, int kk, int Nb, int64_t BH, int N);
+inline bool mask_uses_probe2(const MaskProblem& p) {
+#ifdef BLADE_PROBE_V1  // timing experiment: the round-1 probe on gathered copies
+  return false;
+#else
+  return probe2_supported(p.d, p.kk, p.Nb, p.BH, p.N);
+#endif
+}
 
 inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   MaskWorkspace w{};
@@ -38,9 +49,12 @@ inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   const size_t nk = size_t(p.Nb) * p.kk;              // padded sampled rows / unit
   const size_t ck = 128;  // sampled keys per refine work item (RF_CK)
   w.nchunks = int((nk + ck - 1) / ck);
+  w.nkpad = int((nk + 127) / 128 * 128);
+  const size_t gath = size_t(p.BH) * nk * p.d * 2;  // gathered sampled rows
   size_t o = 0;
-  w.off_qs = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);
-  w.off_ks = o;       o = align256(o + size_t(p.BH) * nk * p.d * 2);
+  w.off_srow = o;     o = align256(o + size_t(p.BH) * 2 * w.nkpad * 4);
+  w.off_qs = o;       o = align256(o + gath);
+  w.off_ks = o;       o = align256(o + gath);
   w.off_pimp = o;     o = align256(o + rows * p.Nb * 4);
   w.off_counters = o; o = align256(o + 64);
   w.off_flags = o;    o = align256(o + rows * 4);
@@ -73,6 +87,8 @@ struct ProbeSelect {
 
 bool probe_tc_supported(int d, int kk, int Nb);
 bool probe_tc_selects();  // selection fused into the probe epilogue?
+cudaError_t launch_probe2(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
+                          const void* qs, const void* ks, float* pimp, cudaStream_t stream);
 cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
                             const void* qs, const void* ks, float* pimp, const ProbeSelect* sel,
                             cudaStream_t stream);

@@ -80,27 +80,43 @@ BLADE_DEVINL void bitonic_pairs(uint64_t (&r)[E], int (&o)[E], int lane) {
 // ---------------------------------------------------------------------------
 // K-mask.1  sampling + gather
 // ---------------------------------------------------------------------------
-template <int D>
+// One warp per (unit, block, Q|K).  Every shuffle runs in warp-converged
+// code (no data-dependent branch around a collective: the compiler would wrap
+// each in a WARPSYNC / ENDCOLLECTIVE sequence); whole warps past the end only
+// skip their memory accesses.
+//
+// kSmallK (k <= 16): only offsets whose hash lies below a threshold T can be
+// among the k_i smallest when at least k_i hashes do; with T / 2^64 = 40 /
+// valid about 40 candidates survive, sorted 2 per lane instead of all 128.
+// Exact: the k_i smallest (hash, offset) pairs of all offsets are the k_i
+// smallest of the candidates whenever there are >= k_i of them.  Otherwise
+// (fewer than k_i, or more than 64 candidates: ~1e-6 per block) lane 0 selects
+// serially from all offsets.  Larger k: the full 128-pair sort.
+template <int D, bool kSmallK>
 __global__ void __launch_bounds__(256) sample_gather_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, int64_t BH,
     int N, int Nb, int b, int kk, uint64_t seed, int mode, int share_qk, int64_t unit_offset,
-    int32_t* __restrict__ sample_idx, __nv_bfloat16* __restrict__ qs,
-    __nv_bfloat16* __restrict__ ks, int* __restrict__ counters) {
+    int32_t* __restrict__ sample_idx, int32_t* __restrict__ srow, int nkpad,
+    __nv_bfloat16* __restrict__ qs, __nv_bfloat16* __restrict__ ks, int* __restrict__ counters) {
   __shared__ int offs[8][128];
+  __shared__ uint32_t sel_bits[8][4];
+  __shared__ uint64_t cand_h[8][64];
+  __shared__ int cand_o[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * 8 + warp;
   if (w == 0 && lane == 0) counters[0] = 0;  // refine queue length
-  if (w >= BH * Nb * 2) return;
+  const bool active = w < BH * Nb * 2;
   const int which = int(w & 1);
   const int64_t rest = w >> 1;
   const int i = int(rest % Nb);
-  const int64_t u = rest / Nb;
+  const int64_t u = active ? rest / Nb : 0;
   const int valid = min(b, N - i * b);
   const int ki = min(kk, valid);
-  int32_t* sidx = sample_idx ? sample_idx + ((u * 2 + which) * Nb + i) * kk : nullptr;
+  int32_t* sidx = sample_idx && active ? sample_idx + ((u * 2 + which) * Nb + i) * kk : nullptr;
 
   if (mode == 2) {
-    for (int p = lane; p < ki; p += 32) offs[warp][p] = sidx[p];
+    if (active)
+      for (int p = lane; p < ki; p += 32) offs[warp][p] = sidx[p];
   } else if (mode == 1) {
     for (int p = lane; p < ki; p += 32)
       offs[warp][p] = int((int64_t(2 * p + 1) * valid) / (2 * ki));
@@ -108,19 +124,9 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
     const int wh = share_qk ? 0 : which;
     const uint64_t key =
         smix(smix(smix(seed, uint64_t(unit_offset + u)), uint64_t(i)), uint64_t(wh));
-    __shared__ uint32_t sel_bits[8][4];
-    __shared__ uint64_t cand_h[8][64];
-    __shared__ int cand_o[8][64];
     if (lane < 4) sel_bits[warp][lane] = 0u;
-    // Fast path (k_i <= 16): only offsets whose hash lies below a threshold
-    // T can be among the k_i smallest when at least k_i hashes do; with
-    // T / 2^64 = 40 / valid about 40 candidates survive (>= 16 and <= 64
-    // except with probability ~1e-5), which are sorted 2 per lane instead of
-    // all 128.  Exact: the k_i smallest (hash, offset) pairs of all offsets are
-    // the k_i smallest of the candidates whenever there are >= k_i of them;
-    // otherwise (or > 64) the full 128-pair sort below runs.
-    bool fast = false;
-    if (ki <= 16) {
+    __syncwarp();
+    if constexpr (kSmallK) {
       const uint64_t T = valid <= 40 ? ~0ull
                                      : uint64_t(40.0 / double(valid) * 18446744073709551616.0);
       uint64_t h[4];
@@ -135,30 +141,47 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
         pos[e] = cnt + __popc(bal & ((1u << lane) - 1u));
         cnt += __popc(bal);
       }
-      if (cnt >= ki && cnt <= 64) {
+      const bool fast = cnt >= ki && cnt <= 64;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (c[e]) {
-            cand_h[warp][pos[e]] = h[e];
-            cand_o[warp][pos[e]] = lane + 32 * e;
-          }
-        __syncwarp();
-        uint64_t r[2];
-        int o[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int x = lane * 2 + e;
-          r[e] = x < cnt ? cand_h[warp][x] : ~0ull;
-          o[e] = x < cnt ? cand_o[warp][x] : 1024 + x;  // pads sort last
+      for (int e = 0; e < 4; ++e)
+        if (c[e] && pos[e] < 64) {
+          cand_h[warp][pos[e]] = h[e];
+          cand_o[warp][pos[e]] = lane + 32 * e;
         }
-        bitonic_pairs<2>(r, o, lane);
+      __syncwarp();
+      uint64_t r[2];
+      int o[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int x = lane * 2 + e;
+        r[e] = x < cnt ? cand_h[warp][x] : ~0ull;
+        o[e] = x < cnt ? cand_o[warp][x] : 1024 + x;  // pads sort last
+      }
+      bitonic_pairs<2>(r, o, lane);  // unconditional: converged shuffles
+      if (fast) {
 #pragma unroll
         for (int e = 0; e < 2; ++e)
           if (lane * 2 + e < ki) atomicOr(&sel_bits[warp][o[e] >> 5], 1u << (o[e] & 31));
-        fast = true;
+      } else if (lane == 0) {  // rare: k_i smallest of all offsets, serially
+        uint64_t last_h = 0;
+        int last_o = -1;
+        for (int n = 0; n < ki; ++n) {
+          uint64_t bh = ~0ull;
+          int bo = 1 << 30;
+          for (int oo = 0; oo < valid; ++oo) {
+            const uint64_t hh = smix(key, uint64_t(oo));
+            const bool after = hh > last_h || (hh == last_h && oo > last_o);
+            if (after && (hh < bh || (hh == bh && oo < bo))) {
+              bh = hh;
+              bo = oo;
+            }
+          }
+          sel_bits[warp][bo >> 5] |= 1u << (bo & 31);
+          last_h = bh;
+          last_o = bo;
+        }
       }
-    }
-    if (!fast) {
+    } else {
       // bitonic sort of the 128 (hash, offset) pairs, ascending; 4 per lane at
       // positions x = 4*lane + e; invalid offsets carry the maximal hash and
       // their (larger) offset, so they sort after every valid one
@@ -170,7 +193,6 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
         r[e] = o[e] < valid ? smix(key, uint64_t(o[e])) : ~0ull;
       }
       bitonic_pairs<4>(r, o, lane);
-      __syncwarp();
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (lane * 4 + e < ki) atomicOr(&sel_bits[warp][o[e] >> 5], 1u << (o[e] & 31));
@@ -180,15 +202,24 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
     __syncwarp();
     int base = 0;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t bits = sel_bits[warp][w];
-      if ((bits >> lane) & 1u) offs[warp][base + __popc(bits & ((1u << lane) - 1u))] = w * 32 + lane;
+    for (int ww = 0; ww < 4; ++ww) {
+      const uint32_t bits = sel_bits[warp][ww];
+      if ((bits >> lane) & 1u) offs[warp][base + __popc(bits & ((1u << lane) - 1u))] = ww * 32 + lane;
       base += __popc(bits);
     }
   }
+  if (!active) return;
   __syncwarp();
   if (sidx && mode != 2)
     for (int p = lane; p < kk; p += 32) sidx[p] = p < ki ? offs[warp][p] : -1;
+  // row index table for the fp64 refinement (K-mask.4): in-unit
+  // row of every sampled slot (block-major), -1 for padding slots; the last
+  // block's warp also pads the table to whole 128-slot tiles
+  int32_t* tab = srow + (u * 2 + which) * int64_t(nkpad);
+  for (int p = lane; p < kk; p += 32) tab[i * kk + p] = p < ki ? i * b + offs[warp][p] : -1;
+  if (i == Nb - 1)
+    for (int x = Nb * kk + lane; x < nkpad; x += 32) tab[x] = -1;
+  if (!qs) return;  // the probe gathers the rows itself (probe2.cu)
 
   // gather rows (16-byte vectors); rows p >= ki are zero
   const __nv_bfloat16* src = (which == 0 ? q : k) + (u * N + int64_t(i) * b) * D;
@@ -420,107 +451,6 @@ BLADE_DEVINL unsigned long long gtime() {
 }
 #endif
 
-// Alg. 1 l.7-10 for one refined row by the whole CTA, in fp64:
-// Z = sum_j P_imp (block reduction), p~_j = P_imp_j / Z (l.7); the rank of
-// each p~_j in the order (p~ desc, id asc) (l.8, reading R-7) by counting, so
-// the selection order is the oracle's exactly; C_m by a block scan of the
-// sorted values, m0 = first m with C_m >= tau (N_b if none or tau >= 1,
-// reading R-4), m = clamp(m0, lo, hi) (l.9); kept = rank < m, compacted in
-// ascending id order (l.10).  Summation orders differ from the oracle's
-// sequential sums only by fp64 rounding (~1e-16), far inside the 1e-6 tie band.
-template <int NT>
-__device__ void refine_select_cta(double* p, double* sorted, int* rank, double* scan, int* cnt,
-                                  int Nb, double tau, int lo, int hi, uint8_t* mask_row,
-                                  int32_t* kv_idx_row, int32_t* kv_cnt_out) {
-  const int tid = threadIdx.x;
-  constexpr int PER = kMaxNb / NT;  // items per thread (Nb <= kMaxNb)
-  // Z
-  double z = 0.0;
-  for (int j = tid; j < Nb; j += NT) z += p[j];
-  scan[tid] = z;
-  __syncthreads();
-  for (int o = NT / 2; o > 0; o >>= 1) {
-    if (tid < o) scan[tid] += scan[tid + o];
-    __syncthreads();
-  }
-  const double Z = scan[0];
-  __syncthreads();
-  for (int j = tid; j < Nb; j += NT) p[j] = p[j] / Z;
-  __syncthreads();
-  // ranks and the sorted row
-  for (int j = tid; j < Nb; j += NT) {
-    const double v = p[j];
-    int r = 0;
-    for (int k = 0; k < Nb; ++k) {
-      const double w = p[k];
-      r += (w > v || (w == v && k < j)) ? 1 : 0;
-    }
-    rank[j] = r;
-    sorted[r] = v;
-  }
-  __syncthreads();
-  // C_m: thread t owns sorted positions [t PER, (t+1) PER)
-  double c[PER];
-  double run = 0.0;
-#pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int x = tid * PER + e;
-    run += x < Nb ? sorted[x] : 0.0;
-    c[e] = run;
-  }
-  scan[tid] = run;
-  __syncthreads();
-  for (int o = 1; o < NT; o <<= 1) {  // inclusive Hillis-Steele scan of the thread totals
-    const double add = tid >= o ? scan[tid - o] : 0.0;
-    __syncthreads();
-    scan[tid] += add;
-    __syncthreads();
-  }
-  const double base = tid > 0 ? scan[tid - 1] : 0.0;
-  int first = Nb + 1;
-#pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int x = tid * PER + e;
-    if (x < Nb && base + c[e] >= tau && first > Nb) first = x + 1;
-  }
-  cnt[tid] = first;
-  __syncthreads();
-  for (int o = NT / 2; o > 0; o >>= 1) {
-    if (tid < o) cnt[tid] = min(cnt[tid], cnt[tid + o]);
-    __syncthreads();
-  }
-  const int m0 = (tau >= 1.0 || cnt[0] > Nb) ? Nb : cnt[0];
-  const int m = min(max(m0, lo), hi);
-  __syncthreads();
-  // l.10: kept = rank < m, ascending ids: block-contiguous ranges of j per thread
-  int kept_here = 0;
-#pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int j = tid * PER + e;
-    if (j < Nb && rank[j] < m) ++kept_here;
-  }
-  cnt[tid] = kept_here;
-  __syncthreads();
-  for (int o = 1; o < NT; o <<= 1) {
-    const int add = tid >= o ? cnt[tid - o] : 0;
-    __syncthreads();
-    cnt[tid] += add;
-    __syncthreads();
-  }
-  int pos = cnt[tid] - kept_here;
-#pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int j = tid * PER + e;
-    if (j < Nb) {
-      const bool keep = rank[j] < m;
-      if (mask_row) mask_row[j] = keep ? 1 : 0;
-      if (keep) kv_idx_row[pos++] = j;
-    }
-  }
-  for (int x = m + tid; x < Nb; x += NT) kv_idx_row[x] = -1;
-  if (tid == 0) *kv_cnt_out = m;
-}
-
 // K-mask.4 on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64).  One CTA
 // (4 warps) per (queued row, chunk of 128 sampled keys), persistent grid.
 // The chunk's 128 key rows (bf16) are staged in shared memory once; warp w
@@ -535,7 +465,7 @@ __device__ void refine_select_cta(double* p, double* sorted, int* rank, double* 
 // and l_c = sum exp(L - M_c).  The CTA that finishes a row's last chunk
 // combines them (Alg. 3 l.14: M = max M_c, l = sum l_c e^{M_c - M}), forms
 // the fp64 P_imp row (l.17-19) and reselects it.  The reselection works on
-// the fp64 values (refine_select_cta).
+// the fp64 values (one warp, select.cuh RowSelect<E, double>).
 constexpr int RF_CK = 128;  // sampled keys per work item
 
 BLADE_DEVINL void dmma_m8n8k4(double (&c)[2], double a, double b) {
@@ -544,12 +474,22 @@ BLADE_DEVINL void dmma_m8n8k4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-BLADE_DEVINL double bf16_lo_f64(uint32_t w) { return double(__uint_as_float(w << 16)); }
-BLADE_DEVINL double bf16_hi_f64(uint32_t w) { return double(__uint_as_float(w & 0xffff0000u)); }
+// bf16 -> fp64 with integer ops (ALU pipe; the F2F.F64 conversion runs on the
+// narrow XU pipe and bound this kernel): exponent rebias 127 -> 1023, the 7
+// mantissa bits on top of the 52; exact for every finite normal bf16, zero
+// and bf16 subnormals (|x| < 1.2e-38, never in a logit that matters) -> +-0.
+BLADE_DEVINL double bf16bits_f64(uint32_t h16) {
+  const uint32_t t = h16 & 0x7fffu;
+  const uint32_t hi = (t >= 0x80u ? t * 8192u + 0x38000000u : 0u) | ((h16 & 0x8000u) << 16);
+  return __hiloint2double(int(hi), 0);
+}
+BLADE_DEVINL double bf16_lo_f64(uint32_t w) { return bf16bits_f64(w & 0xffffu); }
+BLADE_DEVINL double bf16_hi_f64(uint32_t w) { return bf16bits_f64(w >> 16); }
 
 template <int D>
 __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
-    const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N, int Nb,
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+    const int32_t* __restrict__ srow, int nkpad, int N, int Nb,
     int b, int kk, double scale, int nchunks, double tau, int lo, int hi,
     const int* __restrict__ counters, const int32_t* __restrict__ flags, int* __restrict__ done,
     double* __restrict__ r64, double* __restrict__ mpart, double* __restrict__ lpart,
@@ -561,17 +501,14 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
   // the staged key rows; the last CTA of a row reuses the space for the
   // combine (P_imp row, sorted row, ranks) once every warp is past the MMA
   __shared__ __align__(16) char sK[RF_CK * RS];
-  static_assert(RF_CK * RS >= kMaxNb * (8 + 8 + 4), "combine scratch must fit in sK");
+  static_assert(RF_CK * RS >= kMaxNb * 8 + 64, "combine scratch must fit in sK");
   double* sRow = reinterpret_cast<double*>(sK);    // refined P_imp row, then p~ (l.7)
-  double* sSorted = sRow + kMaxNb;                 // p~ in selection order (l.8)
-  int* sRank = reinterpret_cast<int*>(sSorted + kMaxNb);
+  int* sRank = reinterpret_cast<int*>(sRow + kMaxNb);  // warp 0's selection bitmap
   __shared__ __align__(16) char sQ[16 * RS];
   __shared__ double sRg[8][16];    // [16-key group][s] group max / combine scratch
   __shared__ double sW[4][16];     // per-warp partials
   __shared__ double sMc[16];
   __shared__ double sMs[128];
-  __shared__ double sScan[RF_THREADS];
-  __shared__ int sCnt[RF_THREADS];
   __shared__ int last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g8 = lane >> 2, kl = lane & 3;
@@ -594,13 +531,16 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     const int64_t u = row / Nb;
     const int i = int(row % Nb);
     const int ki = min(kk, min(b, N - i * b));
+    const int32_t* srow_q = srow + (u * 2 + 0) * int64_t(nkpad);
+    const int32_t* srow_k = srow + (u * 2 + 1) * int64_t(nkpad);
     __syncthreads();  // the previous item's smem reads are done
     // stage the chunk's key rows (zero past N_k)
     for (int e = tid; e < RF_CK * (D / 8); e += RF_THREADS) {
       const int t = e / (D / 8), v8 = e % (D / 8);
       const int key = c * RF_CK + t;
       uint4 val = make_uint4(0, 0, 0, 0);
-      if (key < NK) val = *reinterpret_cast<const uint4*>(ks + (u * NK + key) * int64_t(D) + v8 * 8);
+      const int kr = key < NK ? srow_k[key] : -1;
+      if (kr >= 0) val = *reinterpret_cast<const uint4*>(k + (u * N + kr) * int64_t(D) + v8 * 8);
       *reinterpret_cast<uint4*>(sK + t * RS + v8 * 16) = val;
     }
     __syncthreads();
@@ -619,8 +559,10 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
       __syncthreads();
       for (int e = tid; e < 16 * (D / 8); e += RF_THREADS) {
         const int s = e / (D / 8), v8 = e % (D / 8);
-        const uint4 val = *reinterpret_cast<const uint4*>(
-            qs + (u * NK + int64_t(i) * kk + sg + s) * D + v8 * 8);
+        const int qr = srow_q[i * kk + sg + s];
+        const uint4 val = qr >= 0 ? *reinterpret_cast<const uint4*>(q + (u * N + qr) * int64_t(D) +
+                                                                    v8 * 8)
+                                  : make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(sQ + s * RS + v8 * 16) = val;
       }
       __syncthreads();
@@ -806,8 +748,23 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
 #ifdef BLADE_RF_TIMING
     const unsigned long long t_sel = gtime();
 #endif
-    refine_select_cta<RF_THREADS>(sRow, sSorted, sRank, sScan, sCnt, Nb, tau, lo, hi,
-                      mask ? mask + row * Nb : nullptr, kv_idx + row * Nb, kv_cnt + row);
+    // l.7-10 in fp64 by one warp (register bitonic sort; select.cuh)
+    if (warp == 0) {
+      uint8_t* mrow = mask ? mask + row * Nb : nullptr;
+      uint32_t* kb = reinterpret_cast<uint32_t*>(sRank);
+      if (Nb <= 64)
+        RowSelect<2, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
+                                  kv_cnt + row, kb);
+      else if (Nb <= 128)
+        RowSelect<4, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
+                                  kv_cnt + row, kb);
+      else if (Nb <= 256)
+        RowSelect<8, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
+                                  kv_cnt + row, kb);
+      else
+        RowSelect<16, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
+                                   kv_cnt + row, kb);
+    }
 #ifdef BLADE_RF_TIMING
     if (tid == 0) {
       const unsigned long long t_done = gtime();
@@ -840,14 +797,24 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   const int64_t rows = p.BH * p.Nb;
   cudaError_t e;
 
-  {  // K-mask.1
+  int32_t* srow = reinterpret_cast<int32_t*>(ws + w.off_srow);
+  const bool p2 = mask_uses_probe2(p);
+  {  // K-mask.1 (sampling, row tables, gathered copies)
     const int64_t warps = p.BH * p.Nb * 2;
-    sample_gather_kernel<D><<<unsigned((warps + 7) / 8), 256, 0, stream>>>(
+    auto kern = p.kk <= 16 ? sample_gather_kernel<D, true> : sample_gather_kernel<D, false>;
+    kern<<<unsigned((warps + 7) / 8), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
-        p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
-        ks, counters);
+        p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, srow,
+        w.nkpad, qs, ks, counters);
   }
-  if (probe_tc_supported(D, p.kk, p.Nb)) {
+  if (p2) {
+    // K-mask.2: tcgen05 probe, even / odd tiles on two warp halves (probe2.cu)
+    e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
+    if (e != cudaSuccess) return e;
+    select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
+        pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
+        done, p.neg_flagged);
+  } else   if (probe_tc_supported(D, p.kk, p.Nb)) {
     // K-mask.2 + K-mask.3 fused: tcgen05 probe, selection in its epilogue
     ProbeSelect ps{p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done,
                    p.neg_flagged};
@@ -882,7 +849,8 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
   refine_kernel<D><<<148 * 3, RF_THREADS, 0, stream>>>(
-      qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k), srow,
+      w.nkpad, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
       flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
 #ifdef BLADE_RF_TIMING
   {

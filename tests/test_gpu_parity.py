@@ -181,4 +181,12 @@ def test_refine_path_every_row(A, case):
     Nb = O.num_blocks(N, 128)
     assert int(got.n_refined.item()) >= H * Nb - H  # rows with m = N_b may skip (T2 needs m < N_b)
     PT.check_mask(ref, got, p)
-    np.testing.assert_allclose(got.p_imp.cpu().numpy(), ref.p_imp, rtol=1e-7, atol=0)
+    # refined rows: the fp64 P_imp rounded to fp32 (1e-7); a row that keeps every
+    # block (m = N_b) has no decision to refine and carries the fp32 probe's own
+    # error (R-14: max measured ~2e-6, refine guard 1e-5)
+    got_p = got.p_imp.cpu().numpy()
+    for i in range(Nb):
+        full = np.array([ref.rows[u][i].m == Nb for u in range(H)])
+        tol = np.where(full, 5e-6, 1e-7)[:, None]
+        err = np.abs(got_p[:, i, :] - ref.p_imp[:, i, :]) / np.abs(ref.p_imp[:, i, :])
+        assert (err <= tol).all(), (i, err.max())
