@@ -481,7 +481,8 @@ def measure_layer(args, workload: str, dev, local: int, *, headline: bool):
     torch.cuda.synchronize()
     clocks = clk.stop() if clk else None
     two_ms = statistics.mean(starts[s].elapsed_time(ends[s]) for s in range(args.steps))
-    attn_ms = statistics.mean(mids[s].elapsed_time(ends[s]) for s in range(args.steps))
+    attn_all = [mids[s].elapsed_time(ends[s]) for s in range(args.steps)]
+    attn_ms = statistics.mean(attn_all)
     mask_ms = statistics.mean(starts[s].elapsed_time(mids[s]) for s in range(args.steps))
     pk, pk_src = peaks()
     attn_tflops = flop / (attn_ms * 1e-3) / 1e12
@@ -490,7 +491,8 @@ def measure_layer(args, workload: str, dev, local: int, *, headline: bool):
            "ms_per_step_two_calls": two_ms, "sparsity": round(float(sparsity), 4),
            "rows_refined_fp64": refined, "mask": mode, "keep": [mp["keep_min"], mp["keep_max"]],
            "attn_tflops": attn_tflops, "attn_frac": attn_tflops / pk["bf16_tflops"],
-           "active_tflop": flop / 1e12, "steps": args.steps}
+           "active_tflop": flop / 1e12, "steps": args.steps,
+           "ms_attn_min_median_max": [min(attn_all), statistics.median(attn_all), max(attn_all)]}
     if not headline:
         return res
     # e2e: host buffers through the ABI, copies inside the timed region
@@ -584,6 +586,7 @@ def run_single(args, dev, local):
                    "rows_refined_fp64": r["rows_refined_fp64"],
                    "probe_gflop": probe_flop(r["BH"], r["N"], r["d"]) / 1e9},
         "ms_mask": r["ms_mask"], "ms_attn": r["ms_attn"],
+        "ms_attn_min_median_max": r["ms_attn_min_median_max"],
         "ms_per_step_two_calls": r["ms_per_step_two_calls"],
         "step_api": ("blade_asa_gt_fwd" if gt else "blade_asa_fwd") +
                     " (one call; attention a programmatic dependent of the mask's last kernel)",

@@ -25,10 +25,9 @@ struct MaskProblem {
 
 // Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
 struct MaskWorkspace {
-  size_t off_srow, off_qs, off_ks, off_pimp, off_counters, off_flags, off_done, off_r64,
+  size_t off_qs, off_ks, off_pimp, off_counters, off_flags, off_done, off_r64,
       off_mpart, off_lpart, total;
   int nchunks;  // refine key chunks of 128 sampled keys
-  int nkpad;    // sampled slots per unit padded to whole 128-slot tiles
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -49,10 +48,8 @@ inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   const size_t nk = size_t(p.Nb) * p.kk;              // padded sampled rows / unit
   const size_t ck = 128;  // sampled keys per refine work item (RF_CK)
   w.nchunks = int((nk + ck - 1) / ck);
-  w.nkpad = int((nk + 127) / 128 * 128);
   const size_t gath = size_t(p.BH) * nk * p.d * 2;  // gathered sampled rows
   size_t o = 0;
-  w.off_srow = o;     o = align256(o + size_t(p.BH) * 2 * w.nkpad * 4);
   w.off_qs = o;       o = align256(o + gath);
   w.off_ks = o;       o = align256(o + gath);
   w.off_pimp = o;     o = align256(o + rows * p.Nb * 4);

@@ -96,8 +96,8 @@ template <int D, bool kSmallK>
 __global__ void __launch_bounds__(256) sample_gather_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, int64_t BH,
     int N, int Nb, int b, int kk, uint64_t seed, int mode, int share_qk, int64_t unit_offset,
-    int32_t* __restrict__ sample_idx, int32_t* __restrict__ srow, int nkpad,
-    __nv_bfloat16* __restrict__ qs, __nv_bfloat16* __restrict__ ks, int* __restrict__ counters) {
+    int32_t* __restrict__ sample_idx, __nv_bfloat16* __restrict__ qs,
+    __nv_bfloat16* __restrict__ ks, int* __restrict__ counters) {
   __shared__ int offs[8][128];
   __shared__ uint32_t sel_bits[8][4];
   __shared__ uint64_t cand_h[8][64];
@@ -212,15 +212,6 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
   __syncwarp();
   if (sidx && mode != 2)
     for (int p = lane; p < kk; p += 32) sidx[p] = p < ki ? offs[warp][p] : -1;
-  // row index table for the fp64 refinement (K-mask.4): in-unit
-  // row of every sampled slot (block-major), -1 for padding slots; the last
-  // block's warp also pads the table to whole 128-slot tiles
-  int32_t* tab = srow + (u * 2 + which) * int64_t(nkpad);
-  for (int p = lane; p < kk; p += 32) tab[i * kk + p] = p < ki ? i * b + offs[warp][p] : -1;
-  if (i == Nb - 1)
-    for (int x = Nb * kk + lane; x < nkpad; x += 32) tab[x] = -1;
-  if (!qs) return;  // the probe gathers the rows itself (probe2.cu)
-
   // gather rows (16-byte vectors); rows p >= ki are zero
   const __nv_bfloat16* src = (which == 0 ? q : k) + (u * N + int64_t(i) * b) * D;
   __nv_bfloat16* dst = (which == 0 ? qs : ks) + (u * int64_t(Nb) * kk + int64_t(i) * kk) * D;
@@ -451,6 +442,120 @@ BLADE_DEVINL unsigned long long gtime() {
 }
 #endif
 
+// Alg. 1 l.7-10 for one refined row by a CTA of NT threads, in
+// fp64: Z = sum_j P_imp (l.7); a bitonic sort of (p~, id) in shared memory,
+// descending with ties by ascending id (l.8, reading R-7); C_m by a block scan
+// of the sorted values, m0 = first m with C_m >= tau (N_b if none or tau >= 1,
+// reading R-4), m = clamp(m0, lo, hi) (l.9); kept ids compacted ascending
+// (l.10).  Summation orders differ from the oracle's sequential sums only by
+// fp64 rounding (~1e-16), far inside the 1e-6 tie band.  scratch: >= kMaxNb
+// (8 + 4) + NT 8 + 64 bytes of shared memory.
+template <int NT>
+__device__ void cta_select_f64(const double* p, int Nb, double tau, int lo, int hi,
+                               uint8_t* mask_row, int32_t* kv_idx_row, int32_t* kv_cnt_out,
+                               char* scratch) {
+  double* sv = reinterpret_cast<double*>(scratch);          // [kMaxNb] sort values
+  int* si = reinterpret_cast<int*>(sv + kMaxNb);            // [kMaxNb] sort ids
+  double* red = reinterpret_cast<double*>(si + kMaxNb);     // [NT]
+  uint32_t* bits = reinterpret_cast<uint32_t*>(red + NT);   // [16]
+  const int tid = threadIdx.x;
+  int P2 = 1;
+  while (P2 < Nb) P2 <<= 1;
+  double z = 0.0;
+  for (int j = tid; j < Nb; j += NT) z += p[j];
+  red[tid] = z;
+  if (tid < 16) bits[tid] = 0u;
+  __syncthreads();
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  const double Z = red[0];
+  for (int j = tid; j < P2; j += NT) {
+    sv[j] = j < Nb ? p[j] / Z : -1.0;  // pads sort last
+    si[j] = j;
+  }
+  __syncthreads();
+  for (int kb = 2; kb <= P2; kb <<= 1) {
+    for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+      for (int x = tid; x < P2; x += NT) {
+        const int y = x ^ jb;
+        if (y > x) {
+          const double vx = sv[x], vy = sv[y];
+          const int ix = si[x], iy = si[y];
+          const bool x_first = vx > vy || (vx == vy && ix < iy);
+          if (x_first != ((x & kb) == 0)) {
+            sv[x] = vy; sv[y] = vx;
+            si[x] = iy; si[y] = ix;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // C_m: thread t owns sorted positions [t PER, (t+1) PER)
+  constexpr int PER = kMaxNb / NT;
+  double run = 0.0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int x = tid * PER + e;
+    run += x < Nb ? sv[x] : 0.0;
+  }
+  __syncthreads();
+  red[tid] = run;
+  __syncthreads();
+  for (int o = 1; o < NT; o <<= 1) {  // inclusive Hillis-Steele scan of the thread totals
+    const double add = tid >= o ? red[tid - o] : 0.0;
+    __syncthreads();
+    red[tid] += add;
+    __syncthreads();
+  }
+  double c = tid > 0 ? red[tid - 1] : 0.0;
+  int first = Nb + 1;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int x = tid * PER + e;
+    if (x < Nb) {
+      c += sv[x];
+      if (c >= tau && first > Nb) first = x + 1;
+    }
+  }
+  __syncthreads();
+  int* cnt = reinterpret_cast<int*>(red);
+  cnt[tid] = first;
+  __syncthreads();
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    if (tid < o) cnt[tid] = min(cnt[tid], cnt[tid + o]);
+    __syncthreads();
+  }
+  const int m0 = (tau >= 1.0 || cnt[0] > Nb) ? Nb : cnt[0];
+  const int m = min(max(m0, lo), hi);
+  for (int x = tid; x < m; x += NT) atomicOr(&bits[si[x] >> 5], 1u << (si[x] & 31));
+  __syncthreads();
+  if (tid < 32) {  // ascending compaction through the bitmap (one warp, converged)
+    const int nwords = (Nb + 31) >> 5;
+    const uint32_t myw = tid < nwords ? bits[tid] : 0u;
+    const int cw = __popc(myw);
+    int pre = cw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (tid >= o) pre += y;
+    }
+    pre -= cw;
+    uint32_t wv = myw;
+    while (wv) {
+      const int bb = __ffs(wv) - 1;
+      wv &= wv - 1;
+      kv_idx_row[pre++] = tid * 32 + bb;
+    }
+  }
+  for (int x = m + tid; x < Nb; x += NT) kv_idx_row[x] = -1;
+  if (mask_row)
+    for (int j = tid; j < Nb; j += NT) mask_row[j] = (bits[j >> 5] >> (j & 31)) & 1u;
+  if (tid == 0) *kv_cnt_out = m;
+}
+
 // K-mask.4 on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64).  One CTA
 // (4 warps) per (queued row, chunk of 128 sampled keys), persistent grid.
 // The chunk's 128 key rows (bf16) are staged in shared memory once; warp w
@@ -465,7 +570,7 @@ BLADE_DEVINL unsigned long long gtime() {
 // and l_c = sum exp(L - M_c).  The CTA that finishes a row's last chunk
 // combines them (Alg. 3 l.14: M = max M_c, l = sum l_c e^{M_c - M}), forms
 // the fp64 P_imp row (l.17-19) and reselects it.  The reselection works on
-// the fp64 values (one warp, select.cuh RowSelect<E, double>).
+// the fp64 values (the whole CTA, cta_select_f64).
 constexpr int RF_CK = 128;  // sampled keys per work item
 
 BLADE_DEVINL void dmma_m8n8k4(double (&c)[2], double a, double b) {
@@ -488,8 +593,7 @@ BLADE_DEVINL double bf16_hi_f64(uint32_t w) { return bf16bits_f64(w >> 16); }
 
 template <int D>
 __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
-    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
-    const int32_t* __restrict__ srow, int nkpad, int N, int Nb,
+    const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N, int Nb,
     int b, int kk, double scale, int nchunks, double tau, int lo, int hi,
     const int* __restrict__ counters, const int32_t* __restrict__ flags, int* __restrict__ done,
     double* __restrict__ r64, double* __restrict__ mpart, double* __restrict__ lpart,
@@ -501,9 +605,9 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
   // the staged key rows; the last CTA of a row reuses the space for the
   // combine (P_imp row, sorted row, ranks) once every warp is past the MMA
   __shared__ __align__(16) char sK[RF_CK * RS];
-  static_assert(RF_CK * RS >= kMaxNb * 8 + 64, "combine scratch must fit in sK");
+  static_assert(RF_CK * RS >= kMaxNb * 8 + kMaxNb * 12 + RF_THREADS * 8 + 64,
+                "combine scratch must fit in sK");
   double* sRow = reinterpret_cast<double*>(sK);    // refined P_imp row, then p~ (l.7)
-  int* sRank = reinterpret_cast<int*>(sRow + kMaxNb);  // warp 0's selection bitmap
   __shared__ __align__(16) char sQ[16 * RS];
   __shared__ double sRg[8][16];    // [16-key group][s] group max / combine scratch
   __shared__ double sW[4][16];     // per-warp partials
@@ -531,18 +635,18 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     const int64_t u = row / Nb;
     const int i = int(row % Nb);
     const int ki = min(kk, min(b, N - i * b));
-    const int32_t* srow_q = srow + (u * 2 + 0) * int64_t(nkpad);
-    const int32_t* srow_k = srow + (u * 2 + 1) * int64_t(nkpad);
     __syncthreads();  // the previous item's smem reads are done
-    // stage the chunk's key rows (zero past N_k)
+    // stage the chunk's key rows (zero past N_k): asynchronous 16-byte copies,
+    // all in flight at once
     for (int e = tid; e < RF_CK * (D / 8); e += RF_THREADS) {
       const int t = e / (D / 8), v8 = e % (D / 8);
       const int key = c * RF_CK + t;
-      uint4 val = make_uint4(0, 0, 0, 0);
-      const int kr = key < NK ? srow_k[key] : -1;
-      if (kr >= 0) val = *reinterpret_cast<const uint4*>(k + (u * N + kr) * int64_t(D) + v8 * 8);
-      *reinterpret_cast<uint4*>(sK + t * RS + v8 * 16) = val;
+      const bool ok = key < NK;
+      cp_async16(smem_u32(sK + t * RS + v8 * 16),
+                 ks + (u * NK + (ok ? key : 0)) * int64_t(D) + v8 * 8, ok ? 16 : 0);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     // validity of this lane's keys (2 per n-tile): padded samples of a ragged
     // last block and slots past N_k get -inf
@@ -559,12 +663,11 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
       __syncthreads();
       for (int e = tid; e < 16 * (D / 8); e += RF_THREADS) {
         const int s = e / (D / 8), v8 = e % (D / 8);
-        const int qr = srow_q[i * kk + sg + s];
-        const uint4 val = qr >= 0 ? *reinterpret_cast<const uint4*>(q + (u * N + qr) * int64_t(D) +
-                                                                    v8 * 8)
-                                  : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sQ + s * RS + v8 * 16) = val;
+        cp_async16(smem_u32(sQ + s * RS + v8 * 16),
+                   qs + (u * NK + int64_t(i) * kk + sg + s) * D + v8 * 8, 16);
       }
+      cp_async_commit();
+      cp_async_wait<0>();
       __syncthreads();
       double acc[2][4][2];
 #pragma unroll
@@ -748,23 +851,10 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
 #ifdef BLADE_RF_TIMING
     const unsigned long long t_sel = gtime();
 #endif
-    // l.7-10 in fp64 by one warp (register bitonic sort; select.cuh)
-    if (warp == 0) {
-      uint8_t* mrow = mask ? mask + row * Nb : nullptr;
-      uint32_t* kb = reinterpret_cast<uint32_t*>(sRank);
-      if (Nb <= 64)
-        RowSelect<2, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
-                                  kv_cnt + row, kb);
-      else if (Nb <= 128)
-        RowSelect<4, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
-                                  kv_cnt + row, kb);
-      else if (Nb <= 256)
-        RowSelect<8, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
-                                  kv_cnt + row, kb);
-      else
-        RowSelect<16, double>::run(sRow, Nb, tau, lo, hi, 0.0, false, mrow, kv_idx + row * Nb,
-                                   kv_cnt + row, kb);
-    }
+    // l.7-10 in fp64 by the whole CTA (shared-memory bitonic sort)
+    cta_select_f64<RF_THREADS>(sRow, Nb, tau, lo, hi, mask ? mask + row * Nb : nullptr,
+                               kv_idx + row * Nb, kv_cnt + row,
+                               reinterpret_cast<char*>(sRow + kMaxNb));
 #ifdef BLADE_RF_TIMING
     if (tid == 0) {
       const unsigned long long t_done = gtime();
@@ -797,15 +887,14 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   const int64_t rows = p.BH * p.Nb;
   cudaError_t e;
 
-  int32_t* srow = reinterpret_cast<int32_t*>(ws + w.off_srow);
   const bool p2 = mask_uses_probe2(p);
-  {  // K-mask.1 (sampling, row tables, gathered copies)
+  {  // K-mask.1 (sampling + gathered copies Q_s, K_s)
     const int64_t warps = p.BH * p.Nb * 2;
     auto kern = p.kk <= 16 ? sample_gather_kernel<D, true> : sample_gather_kernel<D, false>;
     kern<<<unsigned((warps + 7) / 8), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
-        p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, srow,
-        w.nkpad, qs, ks, counters);
+        p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
+        ks, counters);
   }
   if (p2) {
     // K-mask.2: tcgen05 probe, even / odd tiles on two warp halves (probe2.cu)
@@ -849,8 +938,7 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
   refine_kernel<D><<<148 * 3, RF_THREADS, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k), srow,
-      w.nkpad, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
+      qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
       flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
 #ifdef BLADE_RF_TIMING
   {
