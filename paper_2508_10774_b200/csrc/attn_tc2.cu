@@ -19,9 +19,8 @@
 //   warp  8     tcgen05.mma issuer (one thread) + TMEM allocator
 //   warp  9     TMA producer: Q_A, Q_B, then K tiles in consumption order
 //   warp  10    TMA producer: V tiles in consumption order
-//   warp  11    builds the item tables (I, A \ B, B \ A) before the roles start
-//               (an issuer per block was measured 24 % slower: an issuing
-//               thread blocks at the tensor pipe's pace either way)
+//   warp  11    idle (an issuer per block was measured 24 % slower: an
+//               issuing thread blocks at the tensor pipe's pace either way)
 // TMEM (512 columns): S_A [0,128) S_B [128,256) O_A [256, 256+d) O_B [256+d, 256+2d).
 // P (bf16) overwrites the upper half of its S and is the TMEM A operand of
 // P V; S(n+1) of a block is issued after P V(n) of that block (the tensor
@@ -29,17 +28,7 @@
 // also guarantees that P V(n) finished writing O (no separate wait before a
 // rescale).  Q stays in shared memory (S = Q K^T is an SS MMA).
 // K and V rings are shared by both blocks, filled in the order the MMA issuer
-// consumes them.  Adjacent query blocks keep mostly the same key blocks (62 %
-// of the lists on the Wan inputs), so each CTA first splits its two lists
-// into the common part I = A n B and the exclusive parts A \ B, B \ A (warp
-// 11, bitmaps in shared memory) and orders both blocks' items as
-//   [global-token tiles] [I] [own exclusive blocks]:
-// item k < n_S = n_GT + |I| is the same tile for A and B, loaded once into one
-// ring slot and consumed by S_A(k), S_B(k) (K) and P V_A(k), P V_B(k) (V);
-// later items alternate A B A B ... as before (the shorter list ends first).
-// One TMA load and one shared-memory write then serve both blocks wherever
-// their lists agree.  The order of a block's items only changes the fp32
-// rounding of its online softmax (reading R-17).
+// consumes them: A0 B0 A1 B1 ... (the shorter list simply ends earlier).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -84,17 +73,50 @@ struct Cfg2 {
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
   static constexpr int kOffBar = kOffRingV + kRingV * kTile;
   // bar_q, kfull/kempty, vfull/vempty, per block: s, p, pv
-  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 3 * 2;
-  static constexpr int kOffMisc = kOffBar + kNumBar * 8;  // tmem slot, n_I
-  static constexpr int kOffTab = kOffMisc + 16;           // item tables, 3 x 256 B
-  static constexpr int kOffBits = kOffTab + 3 * 256;      // list bitmaps, 2 x 8 words
-  static constexpr int kSmem = kOffBits + 64 + 1024;      // + alignment slack
+  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 6 * 2;
+  static constexpr int kOffMisc = kOffBar + kNumBar * 8;
+  static constexpr int kSmem = kOffMisc + 16 + 1024;  // + alignment slack
   static constexpr uint32_t kColO = 256;
+  // d = 64 leaves TMEM room for P outside S: P_t at [256 + 2d + 64t, +64), so
+  // S_t(n+1) can be issued as soon as the softmax has read S_t(n).  Parity
+  // green, but measured no faster on the Cog layer (1.05 vs 1.04 ms: the
+  // softmax, not the S round trip, bounds d = 64), so off by default.
+#ifndef BLADE_ATTN2_SEP_P
+#define BLADE_ATTN2_SEP_P 0
+#endif
+  static constexpr bool kSepP = D == 64 && BLADE_ATTN2_SEP_P;
+  static constexpr uint32_t kColP = 256 + 2 * D;
+  // Half-tile S pipeline: S = Q K^T as two N = 64 MMAs (keys [0, 64) "early",
+  // [64, 128) "late") into the two 64-column halves of the block's S region,
+  // which alternate roles tile by tile: E_k (early S of tile k, then P(k))
+  // and L_k (late S of tile k).  S_early(k+1) goes to L_k as soon as the
+  // softmax has read S_late(k), so the softmax of tile k+1 starts on its first
+  // half while the tensor core runs P V(k) and S_late(k+1) (into E_k, after
+  // P V(k) has read P(k)).  The online max is lazy (threshold 2^8) per half;
+  // a late-half rescale also rescales the already stored early-half P.
+  // Parity green but slower (Wan 1.39-1.41 vs 1.155 ms, Cog 1.17 vs 1.04 ms,
+  // interleaved A/B): two N = 64 S MMAs read Q twice, 96 instead of 64 KB of
+  // shared memory per tile for S, and the d = 128 kernel is bound by shared-
+  // memory bandwidth, so off by default.
+#ifndef BLADE_ATTN2_HALF_S
+#define BLADE_ATTN2_HALF_S 0
+#endif
+  static constexpr bool kHalfS = BLADE_ATTN2_HALF_S && !kSepP;
 };
 
 constexpr int kThreads2 = 384;
-constexpr int kShareMaxNb = 256;  // item tables hold 8-bit block ids
 
+#ifdef BLADE_ATTN2_TRACE  // timing experiment: event timeline of one CTA
+__device__ long long g_tr2[12][40];
+#define TR2(ev, n)                                                                         \
+  do {                                                                                     \
+    if (blockIdx.x == 50 && blockIdx.y == 3 && (n) < 40) g_tr2[ev][n] = clock64();          \
+  } while (0)
+#else
+#define TR2(ev, n) \
+  do {             \
+  } while (0)
+#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // Which of every 8 exponential pairs run on the FMA pipe (ex2_poly2) instead
 // of MUFU: 1 in 8 for d = 64, none for d = 128 (interleaved A/B on B200:
@@ -106,31 +128,17 @@ constexpr uint32_t kEmuMask2_64 = BLADE_ATTN2_EMU_MASK, kEmuMask2_128 = BLADE_AT
 constexpr uint32_t kEmuMask2_64 = 0x01, kEmuMask2_128 = 0x00;
 #endif
 
-// The item schedule of a CTA.  Items k < nS are shared by both blocks; later
-// items alternate A, B (the shorter list simply ends earlier).  pos() is the
-// position of block t's item k in the sequence the producers fill the rings
-// with and the issuer drains them in.
-struct Sched {
-  int cntA, cntB;  // items per block (kept blocks + global-token tiles)
-  int nS;          // shared items (0 for a lone last block)
-  BLADE_DEVINL int pos(int t, int k) const {
-    if (k < nS) return k;
-    return nS + (min(k, cntA) - nS) + (min(k, cntB) - nS) + ((t == 1 && k < cntA) ? 1 : 0);
+// Interleaved consumption order of the two blocks' items: A0 B0 A1 B1 ...
+// (when one list is exhausted the other continues alone).  Calls f(t, k) for
+// every item in order.
+template <typename F>
+BLADE_DEVINL void for_each_item(int cntA, int cntB, F&& f) {
+  const int m = cntA > cntB ? cntA : cntB;
+  for (int k = 0; k < m; ++k) {
+    if (k < cntA) f(0, k);
+    if (k < cntB) f(1, k);
   }
-  // calls f(t, k, shared) for every ring position in order
-  template <typename F>
-  BLADE_DEVINL void for_each(F&& f) const {
-    const int m = cntA > cntB ? cntA : cntB;
-    for (int k = 0; k < m; ++k) {
-      if (k < nS) {
-        f(0, k, true);
-      } else {
-        if (k < cntA) f(0, k, false);
-        if (k < cntB) f(1, k, false);
-      }
-    }
-  }
-};
+}
 
 template <int D, bool kDefaultScale, bool kGT>
 __global__ void __launch_bounds__(kThreads2, 1)
@@ -156,12 +164,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint64_t* bar_vempty = bar_vfull + C::kRingV;
   uint64_t* bar_s = bar_vempty + C::kRingV;  // [2] S of block t computed
   uint64_t* bar_p = bar_s + 2;               // [2] P of block t written (4 warp arrivals)
-  uint64_t* bar_pv = bar_p + 2;              // [2] last P V of block t done
+  uint64_t* bar_pv = bar_p + 2;              // [2] P V of block t done
+  uint64_t* bar_sf = bar_pv + 2;             // [2] S of block t read out (kSepP, 4 warps)
+  uint64_t* bar_sl = bar_sf + 2;             // [2] late half of S computed (kHalfS)
+  uint64_t* bar_slf = bar_sl + 2;            // [2] late half of S read out (kHalfS, 4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
-  int* s_nI = reinterpret_cast<int*>(smem + C::kOffMisc + 4);
-  uint8_t* tabI = reinterpret_cast<uint8_t*>(smem + C::kOffTab);  // common blocks (A's order)
-  uint8_t* tabX[2] = {tabI + 256, tabI + 512};                      // exclusive blocks of A, B
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + C::kOffBits);  // [2][8] list bitmaps
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // LPT order (blade_asa_fwd, tau mode): CTA b takes the b-th longest pair
@@ -183,9 +190,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
     cf0 = __ldcg(kv_cnt + u * Nb + i0);
     cf1 = nblk == 2 ? __ldcg(kv_cnt + u * Nb + i0 + 1) : 0;
   }
+  const int cnt0 = cf0 + ngt, cnt1 = nblk == 2 ? cf1 + ngt : 0;
   const int32_t* list0 = kv_idx + (u * Nb + i0) * Nb;
   const int32_t* list1 = list0 + Nb;
-  const bool share = nblk == 2 && Nb <= kShareMaxNb;
 
   if (warp == 9 && lane == 0) {
     tc::mbar_init(bar_q, 1);
@@ -201,149 +208,195 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::mbar_init(bar_s + t, 1);
       tc::mbar_init(bar_p + t, 4);
       tc::mbar_init(bar_pv + t, 1);
+      tc::mbar_init(bar_sf + t, 4);
+      tc::mbar_init(bar_sl + t, 1);
+      tc::mbar_init(bar_slf + t, 4);
     }
     tc::fence_barrier_init();
-    // Q_A, Q_B right away: their latency overlaps the item-table build
-    tc::tma_prefetch_desc(&tmQ);
-    tc::mbar_arrive_expect_tx(bar_q, nblk * C::kTile);
-    for (int t = 0; t < nblk; ++t)
-      for (int p = 0; p < C::kPanels; ++p)
-        tc::tma_load_3d(sQ + t * C::kTile + p * C::kPanel, &tmQ, bar_q, p * 64, (i0 + t) * 128,
-                        int(u));
   }
   if (warp == 8) tc::tmem_alloc<512>(tmem_slot);
-  if (warp == 11) {
-    // ---- item tables: I = A n B in A's order, A \ B, B \ A (any list order) ----
-    int nI = 0;
-    if (share) {
-      // both lists in registers (one L2 round trip), bitmaps, then the split
-      int a[kShareMaxNb / 32], bl[kShareMaxNb / 32];
-#pragma unroll
-      for (int e = 0; e < kShareMaxNb / 32; ++e) {
-        a[e] = 32 * e + lane < cf0 ? ld_list(list0 + 32 * e + lane) : -1;
-        bl[e] = 32 * e + lane < cf1 ? ld_list(list1 + 32 * e + lane) : -1;
-      }
-      if (lane < 16) bits[lane] = 0u;
-      __syncwarp();
-#pragma unroll
-      for (int e = 0; e < kShareMaxNb / 32; ++e) {
-        if (a[e] >= 0) atomicOr(&bits[a[e] >> 5], 1u << (a[e] & 31));
-        if (bl[e] >= 0) atomicOr(&bits[8 + (bl[e] >> 5)], 1u << (bl[e] & 31));
-      }
-      __syncwarp();
-      const uint32_t lt = (1u << lane) - 1u;
-      int nxa = 0, nxb = 0;
-#pragma unroll
-      for (int e = 0; e < kShareMaxNb / 32; ++e) {
-        const int j = a[e];
-        const bool in = j >= 0 && ((bits[8 + (j >> 5)] >> (j & 31)) & 1u);
-        const uint32_t bi = __ballot_sync(0xffffffffu, in);
-        const uint32_t bx = __ballot_sync(0xffffffffu, j >= 0 && !in);
-        if (in) tabI[nI + __popc(bi & lt)] = uint8_t(j);
-        else if (j >= 0) tabX[0][nxa + __popc(bx & lt)] = uint8_t(j);
-        nI += __popc(bi);
-        nxa += __popc(bx);
-        const int jb = bl[e];
-        const bool ex = jb >= 0 && !((bits[jb >> 5] >> (jb & 31)) & 1u);
-        const uint32_t bxb = __ballot_sync(0xffffffffu, ex);
-        if (ex) tabX[1][nxb + __popc(bxb & lt)] = uint8_t(jb);
-        nxb += __popc(bxb);
-      }
-    }
-    if (lane == 0) *s_nI = nI;
-  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
-  const int nI = *s_nI;
-  const int cnt0 = cf0 + ngt, cnt1 = nblk == 2 ? cf1 + ngt : 0;
-  const Sched sch{cnt0, cnt1, nblk == 2 ? ngt + nI : 0};
-  // block id of block t's item k (k >= ngt; the first ngt items are the
-  // global-token tiles): common blocks, then the block's own
-  auto item_block = [&](int t, int k) -> int {
-    const int f = k - ngt;
-    if (!share) return ld_list((t ? list1 : list0) + f);
-    return f < nI ? int(tabI[f]) : int(tabX[t][f - nI]);
-  };
   // registers: the two softmax warpgroups hold a 128-column S row per thread;
   // the issuer / producer warpgroup needs few (2 x 128 x 216 + 128 x 56 <= 64K)
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-    if (warp == 9 || warp == 10) {
-      // ===================== TMA producers (warp 9: Q and K, warp 10: V) =====
-      if (lane == 0) {
-        const bool isK = warp == 9;
-        if (isK) {
-          tc::tma_prefetch_desc(&tmK);
-          if (kGT) tc::tma_prefetch_desc(&tmKg);
-        } else {
-          tc::tma_prefetch_desc(&tmV);
-          if (kGT) tc::tma_prefetch_desc(&tmVg);
-        }
-        const int R = isK ? C::kRingK : C::kRingV;
-        char* ring = isK ? sRingK : sRingV;
-        uint64_t* full = isK ? bar_kfull : bar_vfull;
-        uint64_t* empty = isK ? bar_kempty : bar_vempty;
-        const CUtensorMap* m = isK ? &tmK : &tmV;
-        const CUtensorMap* mg = isK ? &tmKg : &tmVg;
-        int g = 0;
-        sch.for_each([&](int t, int k, bool) {
-          const bool fine = !kGT || k >= ngt;
-          const int row0 = fine ? item_block(t, k) * 128 : k * 128;
-          const int s = g % R;
-          tc::mbar_wait(empty + s, ((g / R) & 1) ^ 1);
-          char* dst = ring + s * C::kTile;
-          tc::mbar_arrive_expect_tx(full + s, C::kTile);
+  if (warp == 9 || warp == 10) {
+    // ===================== TMA producers (warp 9: Q and K, warp 10: V) =====
+    if (lane == 0) {
+      const bool isK = warp == 9;
+      if (isK) {
+        tc::tma_prefetch_desc(&tmQ);
+        tc::tma_prefetch_desc(&tmK);
+        if (kGT) tc::tma_prefetch_desc(&tmKg);
+        tc::mbar_arrive_expect_tx(bar_q, nblk * C::kTile);
+        for (int t = 0; t < nblk; ++t)
           for (int p = 0; p < C::kPanels; ++p)
-            tc::tma_load_3d(dst + p * C::kPanel, fine ? m : mg, full + s, p * 64, row0, int(u));
-          ++g;
-        });
+            tc::tma_load_3d(sQ + t * C::kTile + p * C::kPanel, &tmQ, bar_q, p * 64,
+                            (i0 + t) * 128, int(u));
+      } else {
+        tc::tma_prefetch_desc(&tmV);
+        if (kGT) tc::tma_prefetch_desc(&tmVg);
       }
-    } else if (warp == 8) {
-      // ===================== MMA issuer =====================
-      if (lane == 0) {
-        constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
-        constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
-        const uint32_t qbase = smem_u32(sQ), kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
-        tc::mbar_wait(bar_q, 0);
+      const int R = isK ? C::kRingK : C::kRingV;
+      char* ring = isK ? sRingK : sRingV;
+      uint64_t* full = isK ? bar_kfull : bar_vfull;
+      uint64_t* empty = isK ? bar_kempty : bar_vempty;
+      const CUtensorMap* m = isK ? &tmK : &tmV;
+      const CUtensorMap* mg = isK ? &tmKg : &tmVg;
+      int g = 0;
+      // the next block id of each list is loaded one item ahead, so the L2
+      // latency of the list read overlaps the wait for a free slot
+      int pre0 = cf0 > 0 ? ld_list(list0) : 0, pre1 = cf1 > 0 ? ld_list(list1) : 0;
+      for_each_item(cnt0, cnt1, [&](int t, int k) {
+        const int cf = t ? cf1 : cf0;
+        const bool fine = !kGT || k < cf;
+        const int jb = t ? pre1 : pre0;
+        if (k + 1 < cf) {
+          if (t) pre1 = ld_list(list1 + k + 1);
+          else pre0 = ld_list(list0 + k + 1);
+        }
+        const int s = g % R;
+        tc::mbar_wait(empty + s, ((g / R) & 1) ^ 1);
+        TR2(isK ? 0 : 1, g);
+        const CUtensorMap* mm = fine ? m : mg;
+        const int row0 = fine ? jb * 128 : (k - cf) * 128;
+        char* dst = ring + s * C::kTile;
+#ifdef BLADE_ATTN2_SKIP_LOAD  // timing experiment only: MMA on stale smem
+        (void)mm; (void)row0; (void)dst;
+        tc::mbar_arrive(full + s);
+#else
+        tc::mbar_arrive_expect_tx(full + s, C::kTile);
+        for (int p = 0; p < C::kPanels; ++p)
+          tc::tma_load_3d(dst + p * C::kPanel, mm, full + s, p * 64, row0, int(u));
+#endif
+        ++g;
+      });
+    }
+  } else if (warp == 8) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
+      const uint32_t qbase = smem_u32(sQ), kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
+      int gk = 0, gv = 0;  // ring positions (interleaved order A0 B0 A1 B1 ...)
+      tc::mbar_wait(bar_q, 0);
+      tc::fence_after_sync();
+      auto issue_S = [&](int t, int k) {  // S_t = Q_t K^T of block t's item k
+        const int s = gk % C::kRingK;
+        tc::mbar_wait(bar_kfull + s, (gk / C::kRingK) & 1);
         tc::fence_after_sync();
-        auto issue_S = [&](int t, int k) {  // S_t = Q_t K^T of block t's item k
-          const int g = sch.pos(t, k), s = g % C::kRingK;
-          tc::mbar_wait(bar_kfull + s, (g / C::kRingK) & 1);
-          tc::fence_after_sync();
-          const uint32_t kb = kbase + s * C::kTile, qb = qbase + t * C::kTile;
+        TR2(2 + t, k);
+        const uint32_t kb = kbase + s * C::kTile, qb = qbase + t * C::kTile;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
+          tc::mma_ss(tmem + t * 128, tc::sw128_desc(qb + off, 16, 1024),
+                     tc::sw128_desc(kb + off, 16, 1024), idS, ks > 0);
+        }
+        tc::commit(bar_s + t);
+        tc::commit(bar_kempty + s);
+        ++gk;
+      };
+      auto issue_PV = [&](int t, int k) {  // O_t += P_t V of block t's item k
+        const int s = gv % C::kRingV;
+        tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
+        TR2(8 + t, k);
+        tc::mbar_wait(bar_p + t, k & 1);
+        tc::fence_after_sync();
+        TR2(4 + t, k);
+        const uint32_t vb = vbase + s * C::kTile;
+        const uint32_t pcol = C::kSepP ? C::kColP + t * 64 : t * 128 + 64;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
+                     tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
+                     (k > 0 || ks > 0) ? 1 : 0);
+        // bar_pv: with kSepP the softmax waits for every P V; otherwise only
+        // the last one is awaited (S(n) is issued after P V(n-1), and tcgen05
+        // ops of one thread complete in order), so only the last is committed
+        // and every phase of the barrier has a waiter (compute-sanitizer
+        // synccheck flags a phase nobody waits for)
+        if (C::kSepP || k + 1 == (t ? cnt1 : cnt0)) tc::commit(bar_pv + t);
+        tc::commit(bar_vempty + s);
+        ++gv;
+      };
+      if constexpr (C::kHalfS) {
+        constexpr uint32_t idS64 = tc::idesc_bf16(128, 64, 0, 0);
+        int kslot[2] = {0, 0};
+        // half h of S_t(k) (keys [64h, 64h+64)) into column half `dst` of S_t
+        auto issue_Sh = [&](int t, int k, int h) {
+          if (h == 0) {  // first use of item (t, k)'s K slot
+            const int s = gk % C::kRingK;
+            tc::mbar_wait(bar_kfull + s, (gk / C::kRingK) & 1);
+            tc::fence_after_sync();
+            kslot[t] = s;
+            ++gk;
+          }
+          const int s = kslot[t];
+          const uint32_t kb = kbase + s * C::kTile + h * 8192, qb = qbase + t * C::kTile;
+          const uint32_t dst = t * 128 + ((k & 1) ^ h) * 64;  // early: E_k, late: L_k
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
             const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-            tc::mma_ss(tmem + t * 128, tc::sw128_desc(qb + off, 16, 1024),
-                       tc::sw128_desc(kb + off, 16, 1024), idS, ks > 0);
+            tc::mma_ss(tmem + dst, tc::sw128_desc(qb + off, 16, 1024),
+                       tc::sw128_desc(kb + off, 16, 1024), idS64, ks > 0);
           }
-          tc::commit(bar_s + t);
-          // a shared tile is released after its second reader, S_B(k)
-          if (k >= sch.nS || t == 1) tc::commit(bar_kempty + s);
+          tc::commit(h ? bar_sl + t : bar_s + t);
+          if (h) tc::commit(bar_kempty + s);
         };
-        auto issue_PV = [&](int t, int k) {  // O_t += P_t V of block t's item k
-          const int g = sch.pos(t, k), s = g % C::kRingV;
-          tc::mbar_wait(bar_vfull + s, (g / C::kRingV) & 1);
+        auto issue_PVh = [&](int t, int k) {  // O_t += P_t(k) V, P_t(k) in E_k
+          const int s = gv % C::kRingV;
+          tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
           tc::mbar_wait(bar_p + t, k & 1);
           tc::fence_after_sync();
           const uint32_t vb = vbase + s * C::kTile;
+          const uint32_t pcol = t * 128 + (k & 1) * 64;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
-            tc::mma_ts(tmem + C::kColO + t * D, tmem + t * 128 + 64 + ks * 8,
+            tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
                        tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                        (k > 0 || ks > 0) ? 1 : 0);
-          // only the last P V of a block is awaited (S(n) is issued after P
-          // V(n-1) and tcgen05 ops of one thread complete in order): one
-          // commit, so every phase of bar_pv has a waiter
-          if (k + 1 == (t ? cnt1 : cnt0)) tc::commit(bar_pv + t);
-          if (k >= sch.nS || t == 1) tc::commit(bar_vempty + s);
+          tc::commit(bar_pv + t);
+          tc::commit(bar_vempty + s);
+          ++gv;
         };
-        if (cnt0 > 0) issue_S(0, 0);
-        if (cnt1 > 0) issue_S(1, 0);
+        for (int t = 0; t < 2; ++t)
+          if ((t ? cnt1 : cnt0) > 0) {
+            issue_Sh(t, 0, 0);
+            issue_Sh(t, 0, 1);
+          }
         const int m = cnt0 > cnt1 ? cnt0 : cnt1;
-        for (int k = 0; k < m; ++k) {
+        for (int k = 0; k < m; ++k)
+          for (int t = 0; t < 2; ++t) {
+            const int c = t ? cnt1 : cnt0;
+            if (k >= c) continue;
+            if (k + 1 < c) {  // L_k free once the softmax has read S_late(k)
+              tc::mbar_wait(bar_slf + t, k & 1);
+              issue_Sh(t, k + 1, 0);
+            }
+            issue_PVh(t, k);
+            if (k + 1 < c) issue_Sh(t, k + 1, 1);  // into E_k, after P V(k) read P(k)
+          }
+      } else {
+      if (cnt0 > 0) issue_S(0, 0);
+      if (cnt1 > 0) issue_S(1, 0);
+      const int m = cnt0 > cnt1 ? cnt0 : cnt1;
+      for (int k = 0; k < m; ++k) {
+        if (C::kSepP) {
+          // S(k+1) of both blocks as soon as their S(k) has been read out, then
+          // the P V of item k: the tensor core computes S(k+1) while the
+          // softmax turns S(k) into P(k)
+          for (int t = 0; t < 2; ++t)
+            if (k + 1 < (t ? cnt1 : cnt0)) {
+              tc::mbar_wait(bar_sf + t, k & 1);
+              issue_S(t, k + 1);
+            }
+          if (k < cnt0) issue_PV(0, k);
+          if (k < cnt1) issue_PV(1, k);
+        } else {
           if (k < cnt0) {
             issue_PV(0, k);
             if (k + 1 < cnt0) issue_S(0, k + 1);
@@ -353,26 +406,172 @@ __global__ void __launch_bounds__(kThreads2, 1)
             if (k + 1 < cnt1) issue_S(1, k + 1);
           }
         }
-        // drain: the last commits must land before the CTA's smem is released
-        if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, 0);
-        if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, 0);
       }
+      }  // !kHalfS
+      // drain: the last commits must land before the CTA's smem is released
+      constexpr bool kPvEvery = C::kSepP || C::kHalfS;  // one bar_pv phase per item
+      if (cnt0 > 0) tc::mbar_wait(bar_pv + 0, kPvEvery ? (cnt0 - 1) & 1 : 0);
+      if (cnt1 > 0) tc::mbar_wait(bar_pv + 1, kPvEvery ? (cnt1 - 1) & 1 : 0);
     }
+  }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
     // ===================== softmax of block t =====================
     const int t = warp >> 2, qw = warp & 3;
     const int cnt = t ? cnt1 : cnt0;
+    const int cnt_fine = t ? cf1 : cf0;
+    const int32_t* list = t ? list1 : list0;
     const uint32_t lane_base = uint32_t(qw * 32) << 16;
     const uint32_t tS = tmem + lane_base + t * 128;
     const uint32_t tO = tmem + lane_base + C::kColO + t * D;
     const int r = qw * 32 + lane;
     float m_used = -INFINITY, l_sum = 0.f;
+    int jn = cnt_fine > 0 ? ld_list(list) : 0;  // block id, loaded one tile ahead
+    if constexpr (C::kHalfS) {
+      const float2 sl2 = make_float2(scale_log2, scale_log2);
+      // rescale O_t (and l) by f; O_t must be current
+      auto rescale_o = [&](float f) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t rr[32];
+          tc::ld_32x32b_x32(tO + c * 32, rr);
+          tc::wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * f);
+          tc::st_32x32b_x32(tO + c * 32, rr);
+        }
+      };
+      // 64 scores of half h (keys [64h, 64h+64)) from TMEM column base `col`,
+      // masked / biased; returns their max
+      auto load_half = [&](uint32_t col, int h, int n, int jb, float (&x)[64]) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t rr[32];
+          tc::ld_32x32b_x32(col + c * 32, rr);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) x[c * 32 + e] = __uint_as_float(rr[e]);
+        }
+        tc::wait_ld();
+        const bool fine = !kGT || n < cnt_fine;
+        const int valid = (fine ? N - jb * 128 : gt.Ng - (n - cnt_fine) * 128) - 64 * h;
+        if (valid < 64) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c >= valid) x[c] = -INFINITY;
+        }
+        if (kGT && !fine) {
+          const int last = gt.Ng - 1 - (n - cnt_fine) * 128 - 64 * h;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) x[c] += c == last ? gt.bias_last : gt.bias_full;
+        }
+        float t4[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float m4 = fmaxf(x[g], x[g + 4]);
+#pragma unroll
+          for (int c = g + 8; c < 64; c += 8) m4 = fmaxf(m4, fmaxf(x[c], x[c + 4]));
+          t4[g] = m4;
+        }
+        return fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+      };
+      // P = 2^(s scale - m_used) of a half -> packed bf16 columns [32h, 32h+32) of E
+      auto exp_store = [&](const float (&x)[64], uint32_t ecol, int h) {
+        float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
+        const float2 nm = make_float2(-m_used, -m_used);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 xx = fma2(make_float2(x[c * 32 + 2 * e], x[c * 32 + 2 * e + 1]), sl2, nm);
+            float2 pp;
+            if (((D == 64 ? kEmuMask2_64 : kEmuMask2_128) >> (e & 7)) & 1) {
+              pp = ex2_poly2(xx);
+            } else {
+              pp.x = ex2(xx.x);
+              pp.y = ex2(xx.y);
+            }
+            acc4[e & 3] = add2(acc4[e & 3], pp);
+            pk[e] = pack_bf16(pp.x, pp.y);
+          }
+          tc::st_32x32b_x16(ecol + 32 * h + c * 16, pk);
+        }
+        const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
+        l_sum += acc.x + acc.y;
+      };
+      for (int n = 0; n < cnt; ++n) {
+        const int jb = jn;
+        if (n + 1 < cnt_fine) jn = ld_list(list + n + 1);
+        const uint32_t E = tS + (n & 1) * 64, Lc = tS + ((n & 1) ^ 1) * 64;
+        float x[64];
+        // ---- early half (keys [0, 64)) in E_n
+        tc::mbar_wait(bar_s + t, n & 1);
+        tc::fence_after_sync();
+        {
+          const float mxs = load_half(E, 0, n, jb, x) * scale_log2;
+          if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
+            const float m_new = fmaxf(m_used, mxs);
+            if (n > 0) {  // O_t current: P V(n-1) done
+              tc::mbar_wait(bar_pv + t, (n - 1) & 1);
+              tc::fence_after_sync();
+              const float f = ex2(m_used - m_new);
+              l_sum *= f;
+              rescale_o(f);
+            }
+            m_used = m_new;
+          }
+        }
+        exp_store(x, E, 0);
+        // ---- late half (keys [64, 128)) in L_n
+        tc::mbar_wait(bar_sl + t, n & 1);
+        tc::fence_after_sync();
+        {
+          const float mxs = load_half(Lc, 1, n, jb, x) * scale_log2;
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(bar_slf + t);  // L_n may take S_early(n+1)
+          if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
+            // S_late(n) complete => P V(n-1) complete (issued before it)
+            const float m_new = fmaxf(m_used, mxs);
+            const float f = ex2(m_used - m_new);
+            l_sum *= f;
+            if (n > 0) rescale_o(f);
+            tc::wait_st();
+            {  // the early half's P, already stored with the old max
+              uint32_t rr[32];
+              tc::ld_32x32b_x32(E, rr);
+              tc::wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const float2 v = unpack_bf16(rr[e]);
+                rr[e] = pack_bf16(v.x * f, v.y * f);
+              }
+              tc::st_32x32b_x32(E, rr);
+            }
+            m_used = m_new;
+          }
+        }
+        exp_store(x, E, 1);
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar_p + t);
+      }
+    } else
     for (int n = 0; n < cnt; ++n) {
-      const bool fine = !kGT || n >= ngt;
-      const int valid = fine ? N - item_block(t, n) * 128 : gt.Ng - n * 128;
+      const int jb = jn;
+      if (n + 1 < cnt_fine) jn = ld_list(list + n + 1);
       tc::mbar_wait(bar_s + t, n & 1);
       tc::fence_after_sync();
+      if (lane == 0 && qw == 0) TR2(6 + t, n);
+#ifdef BLADE_ATTN2_SKIP_SOFTMAX  // timing experiment only: MMA / TMA pipeline alone
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0 && C::kSepP) tc::mbar_arrive(bar_sf + t);
+      if (lane == 0) tc::mbar_arrive(bar_p + t);
+      continue;
+#endif
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -382,13 +581,20 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
       }
       tc::wait_ld();
+      if (C::kSepP) {  // S_t's columns may be overwritten by S_t(n+1) now
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar_sf + t);
+      }
+      const bool fine = !kGT || n < cnt_fine;
+      const int valid = fine ? N - jb * 128 : gt.Ng - (n - cnt_fine) * 128;
       if (valid < 128) {
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (c >= valid) s[c] = -INFINITY;
       }
       if (kGT && !fine) {  // + ln(n_w) on the pooled region, raw-score units
-        const int last = gt.Ng - 1 - n * 128;
+        const int last = gt.Ng - 1 - (n - cnt_fine) * 128;
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] += c == last ? gt.bias_last : gt.bias_full;
       }
@@ -406,8 +612,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
                    fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
       }
       const float mxs = mx * scale_log2;
+      if (C::kSepP && n > 0) {  // P V_t(n-1) done: O_t current and P_t's columns free
+        tc::mbar_wait(bar_pv + t, (n - 1) & 1);
+        tc::fence_after_sync();
+      }
       // warp-uniform (tcgen05.ld/st are .sync.aligned); always true for n = 0.
-      // O_t is current: S_t(n) was issued after P V_t(n-1) and has completed.
+      // O_t is current (kSepP: waited above; else S_t(n) was issued after
+      // P V_t(n-1) and has completed).
       if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThreshold)) {
         const float m_new = fmaxf(m_used, mxs);
         if (n > 0) {
@@ -445,7 +656,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
           acc4[e & 3] = add2(acc4[e & 3], pp);
           pk[e] = pack_bf16(pp.x, pp.y);
         }
-        tc::st_32x32b_x16(tS + 64 + c * 16, pk);
+        tc::st_32x32b_x16(C::kSepP ? tmem + lane_base + C::kColP + t * 64 + c * 16
+                                   : tS + 64 + c * 16,
+                          pk);
       }
       const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
       l_sum += acc.x + acc.y;
@@ -453,10 +666,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bar_p + t);
+      if (lane == 0 && qw == 0) TR2(10 + t, n);
     }
     if (cnt > 0) {
       // epilogue: O / l -> bf16, LSE
-      tc::mbar_wait(bar_pv + t, 0);
+      tc::mbar_wait(bar_pv + t, (C::kSepP || C::kHalfS) ? (cnt - 1) & 1 : 0);
       tc::fence_after_sync();
       const int row = (i0 + t) * 128 + r;
       const float inv = 1.f / l_sum;
@@ -536,6 +750,22 @@ cudaError_t launch2_d(const AttnProblem& p, const void* q, const void* k, const 
                                             reinterpret_cast<__nv_bfloat16*>(o), lse, 0, order);
   }
   e = cudaGetLastError();
+#ifdef BLADE_ATTN2_TRACE
+  {
+    static int calls = 0;
+    long long h[12][40];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h, g_tr2, sizeof(h));
+    if (++calls == 10) {
+      const long long t0 = h[0][0];
+      fprintf(stderr, "k : Kld Vld | S_A S_B | Vrdy_A PV_A Vrdy_B PV_B | smA_in smA_out smB_in smB_out (cycles)\n");
+      for (int n = 0; n < 24; ++n)
+        fprintf(stderr, "%2d: %6lld %6lld | %6lld %6lld | %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld\n", n,
+                h[0][n] - t0, h[1][n] - t0, h[2][n] - t0, h[3][n] - t0, h[8][n] - t0, h[4][n] - t0,
+                h[9][n] - t0, h[5][n] - t0, h[6][n] - t0, h[10][n] - t0, h[7][n] - t0, h[11][n] - t0);
+    }
+  }
+#endif
   return e;
 }
 
