@@ -110,9 +110,9 @@ size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t bl
 /* Attention implementations (the `impl` argument of blade_bsa_fwd). */
 #define BLADE_ATTN_AUTO 0      /* fastest measured: TCGEN05_PAIR for d = 64 and 128     */
 #define BLADE_ATTN_TCGEN05 1   /* sm_100a tcgen05 + TMEM + TMA warp-specialised kernel */
-#define BLADE_ATTN_MMA_SYNC 2  /* legacy mma.sync baseline (kept for comparison)       */
+#define BLADE_ATTN_MMA_SYNC 2  /* legacy mma.sync baseline (BLADE_WITH_BASELINES builds)  */
 #define BLADE_ATTN_TCGEN05_PAIR 3 /* tcgen05 kernel with two query blocks per CTA (ping-pong) */
-#define BLADE_ATTN_TCGEN05_TRIPLE 4 /* tcgen05 kernel, one query block, three S buffers  */
+#define BLADE_ATTN_TCGEN05_TRIPLE 4 /* one query block, three S buffers (baseline builds) */
 
 /*
  * blade_bsa_fwd — block-sparse attention over kept blocks.
@@ -328,6 +328,13 @@ const char* blade_status_string(blade_status_t status);
 
 /* Library version as 10000*major + 100*minor + patch. */
 int32_t blade_version(void);
+
+/* 1 if attention implementation `impl` (BLADE_ATTN_*) is compiled into this
+ * library, else 0.  The product build has AUTO, TCGEN05 and TCGEN05_PAIR; the
+ * MMA_SYNC and TCGEN05_TRIPLE comparison kernels (and the mma.sync backward)
+ * only exist in -DBLADE_WITH_BASELINES builds; elsewhere they return
+ * BLADE_ERR_UNSUPPORTED. */
+int32_t blade_attn_impl_built(int32_t impl);
 
 #ifdef __cplusplus
 }

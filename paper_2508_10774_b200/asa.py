@@ -36,7 +36,7 @@ ABI_SYMBOLS = ("blade_asa_mask_workspace_size", "blade_asa_mask", "blade_bsa_fwd
                "blade_bsa_gt_bwd_workspace_size", "blade_bsa_gt_bwd", "blade_asa_gt_fwd",
                "blade_gilbert_order", "blade_permute_tokens",
                "blade_asa_fwd_host_workspace_size", "blade_asa_fwd_host",
-               "blade_status_string", "blade_version")
+               "blade_status_string", "blade_version", "blade_attn_impl_built")
 
 
 class BladeAsaParams(ctypes.Structure):
@@ -98,6 +98,8 @@ _lib.blade_asa_fwd_host.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32,
 _lib.blade_status_string.restype = ctypes.c_char_p
 _lib.blade_status_string.argtypes = [ctypes.c_int]
 _lib.blade_version.restype = _i32
+_lib.blade_attn_impl_built.restype = _i32
+_lib.blade_attn_impl_built.argtypes = [_i32]
 
 
 class BladeError(RuntimeError):
@@ -112,6 +114,11 @@ def library_path() -> str:
 
 def version() -> int:
     return int(_lib.blade_version())
+
+
+def impl_built(impl: int) -> bool:
+    """Is attention implementation `impl` compiled into the library?"""
+    return bool(_lib.blade_attn_impl_built(impl))
 
 
 def default_scale(d: int) -> float:

@@ -122,6 +122,7 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   // (interleaved A/B: Cog d = 64 1.038 vs 1.232 ms; Wan d = 128 1.170-1.180 vs
   // 1.181-1.189 ms, fused step 1.37-1.39 vs 1.40-1.43 ms)
   const bool pair = impl == BLADE_ATTN_TCGEN05_PAIR || impl == BLADE_ATTN_AUTO;
+  if (!blade::impl_built(impl)) return BLADE_ERR_UNSUPPORTED;
   if (impl == BLADE_ATTN_MMA_SYNC) {
     e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
   } else if (pair) {
@@ -133,10 +134,7 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   } else {
     e = blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,
                               static_cast<char*>(workspace), workspace_bytes, s);
-    if (e == cudaErrorNotSupported) {
-      if (impl == BLADE_ATTN_TCGEN05) return BLADE_ERR_UNSUPPORTED;
-      e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
-    }
+    if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   }
   return e == cudaSuccess ? BLADE_OK : BLADE_ERR_CUDA;
 }
@@ -164,6 +162,7 @@ blade_status_t asa_fwd_common(const void* q, const void* k, const void* v, int64
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return BLADE_ERR_INVALID_ARG;
   if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
   if (gt && impl == BLADE_ATTN_MMA_SYNC) return BLADE_ERR_UNSUPPORTED;
+  if (!blade::impl_built(impl)) return BLADE_ERR_UNSUPPORTED;
   MaskProblem mp;
   blade_status_t st = make_mask_problem(BH, N, d, params, &mp);
   if (st != BLADE_OK) return st;
@@ -262,7 +261,7 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
     return BLADE_ERR_INVALID_ARG;
   if (impl < BLADE_ATTN_AUTO || impl > BLADE_ATTN_TCGEN05_TRIPLE) return BLADE_ERR_INVALID_ARG;
   if (block != kGpuBlock || (d != 64 && d != 128) || impl == BLADE_ATTN_MMA_SYNC ||
-      BH > kMaxBH)
+      BH > kMaxBH || !blade::impl_built(impl))
     return BLADE_ERR_UNSUPPORTED;
   const int64_t Nb = (int64_t(N) + block - 1) / block;
   if (Nb > kMaxNb) return BLADE_ERR_UNSUPPORTED;
@@ -367,6 +366,8 @@ const char* blade_status_string(blade_status_t status) {
   return "unknown status";
 }
 
-int32_t blade_version(void) { return 100; }
+int32_t blade_version(void) { return 200; }
+
+int32_t blade_attn_impl_built(int32_t impl) { return blade::impl_built(impl) ? 1 : 0; }
 
 }  // extern "C"

@@ -15,10 +15,11 @@
 // The dK/dV and dQ products run in the tcgen05 kernels of attn_bwd_tc.cu;
 // the mma.sync kernels below (FlashAttention-2 structure: CTA = 64 rows, 4
 // warps x 16 rows, 64-row tiles of the other operand double-buffered with
-// cp.async) are the legacy-tensor-path baseline, used when a TMA tensor map
-// cannot be built and selectable with -DBLADE_BWD_{DKDV,DQ}_MMA_SYNC for
-// comparison (12.3 ms vs 3.9 ms on the Wan layer).  P and dS are rounded to
-// bf16 for their MMAs in both.
+// cp.async) are the legacy-tensor-path baseline, compiled only into
+// -DBLADE_WITH_BASELINES builds (selectable there with
+// -DBLADE_BWD_{DKDV,DQ}_MMA_SYNC; 12.3 ms vs 3.9 ms on the Wan layer); the
+// product build returns UNSUPPORTED where a TMA tensor map cannot be built.
+// P and dS are rounded to bf16 for their MMAs in both.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -637,6 +638,22 @@ __global__ void __launch_bounds__(BW_THREADS) gt_bwd_dq_kernel(
   }
 }
 
+#ifdef BLADE_WITH_BASELINES
+constexpr bool kBaselines = true;
+#else
+constexpr bool kBaselines = false;
+#endif
+#if defined(BLADE_WITH_BASELINES) && defined(BLADE_BWD_DKDV_MMA_SYNC)
+constexpr bool kForceDkdvMma = true;
+#else
+constexpr bool kForceDkdvMma = false;
+#endif
+#if defined(BLADE_WITH_BASELINES) && defined(BLADE_BWD_DQ_MMA_SYNC)
+constexpr bool kForceDqMma = true;
+#else
+constexpr bool kForceDqMma = false;
+#endif
+
 template <int D>
 cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, const void* v,
                          const void* o, const float* lse, const void* dout,
@@ -655,23 +672,29 @@ cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, con
   constexpr int TB = BW_TILE * D * 2;
   const int smem_kv = 6 * TB + 4 * BW_TILE * 4;
   const int smem_q = 6 * TB;
-  cudaError_t e = cudaFuncSetAttribute(bsa_bwd_dkdv_kernel<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(bsa_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_q);
-  if (e != cudaSuccess) return e;
   dim3 grid(unsigned(2 * p.Nb), unsigned(p.BH));
+  cudaError_t e;
+  // dK, dV on tcgen05 (attn_bwd_tc.cu); the mma.sync kernels of this file are
+  // compiled only into -DBLADE_WITH_BASELINES builds (comparison baseline, or
+  // -DBLADE_BWD_DKDV_MMA_SYNC / -DBLADE_BWD_DQ_MMA_SYNC to force them)
   bool dkdv_done = false;
-#ifndef BLADE_BWD_DKDV_MMA_SYNC
-  e = launch_bwd_dkdv_tc(p, q, k, v, lse, dout, Dvec, q_idx, q_cnt, dk, dv, stream);
-  if (e != cudaSuccess && e != cudaErrorNotSupported) return e;
-  dkdv_done = e == cudaSuccess;
-#endif
-  if (!dkdv_done)
-    bsa_bwd_dkdv_kernel<D><<<grid, BW_THREADS, smem_kv, stream>>>(
-        B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, q_idx, q_cnt,
-        reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
+  if constexpr (!kForceDkdvMma) {
+    e = launch_bwd_dkdv_tc(p, q, k, v, lse, dout, Dvec, q_idx, q_cnt, dk, dv, stream);
+    if (e != cudaSuccess && e != cudaErrorNotSupported) return e;
+    dkdv_done = e == cudaSuccess;
+  }
+  if (!dkdv_done) {
+    if constexpr (kBaselines) {
+      e = cudaFuncSetAttribute(bsa_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_kv);
+      if (e != cudaSuccess) return e;
+      bsa_bwd_dkdv_kernel<D><<<grid, BW_THREADS, smem_kv, stream>>>(
+          B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, q_idx, q_cnt,
+          reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv));
+    } else {
+      return cudaErrorNotSupported;
+    }
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (gp) {  // dK_g, dV_g partials -> sums / n_w -> spread over the windows
@@ -680,23 +703,27 @@ cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, con
     float* gsum = reinterpret_cast<float*>(ws + gw.off_gsum);
     const int64_t part_stride = int64_t(gw.splits) * p.BH * gw.Ngp * D;
     bool done = false;
-#ifndef BLADE_BWD_DKDV_MMA_SYNC
-    e = launch_bwd_dkdv_tc(p, q, k, v, lse, dout, Dvec, nullptr, nullptr, nullptr, nullptr,
-                           stream, gp, part, gw.splits);
-    if (e != cudaSuccess && e != cudaErrorNotSupported) return e;
-    done = e == cudaSuccess;
-#endif
+    if constexpr (!kForceDkdvMma) {
+      e = launch_bwd_dkdv_tc(p, q, k, v, lse, dout, Dvec, nullptr, nullptr, nullptr, nullptr,
+                             stream, gp, part, gw.splits);
+      if (e != cudaSuccess && e != cudaErrorNotSupported) return e;
+      done = e == cudaSuccess;
+    }
     if (!done) {
-      e = cudaFuncSetAttribute(gt_bwd_dkdv_kernel<D>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
-      if (e != cudaSuccess) return e;
-      const int nqt = (p.N + BW_TILE - 1) / BW_TILE;
-      const int tps = (nqt + gw.splits - 1) / gw.splits;
-      gt_bwd_dkdv_kernel<D><<<dim3(unsigned(gw.Ngp / BW_ROWS), unsigned(p.BH),
-                                   unsigned(gw.splits)),
-                              BW_THREADS, smem_kv, stream>>>(
-          B(q), B(gp->kg), B(gp->vg), B(dout), lse, Dvec, p.N, gp->Ng, gp->window, p.scale, tps,
-          part_stride, part);
+      if constexpr (kBaselines) {
+        e = cudaFuncSetAttribute(gt_bwd_dkdv_kernel<D>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
+        if (e != cudaSuccess) return e;
+        const int nqt = (p.N + BW_TILE - 1) / BW_TILE;
+        const int tps = (nqt + gw.splits - 1) / gw.splits;
+        gt_bwd_dkdv_kernel<D><<<dim3(unsigned(gw.Ngp / BW_ROWS), unsigned(p.BH),
+                                     unsigned(gw.splits)),
+                                BW_THREADS, smem_kv, stream>>>(
+            B(q), B(gp->kg), B(gp->vg), B(dout), lse, Dvec, p.N, gp->Ng, gp->window, p.scale,
+            tps, part_stride, part);
+      } else {
+        return cudaErrorNotSupported;
+      }
     }
     const int64_t nred = 2 * p.BH * gp->Ng * D;
     gt_bwd_reduce_kernel<<<unsigned((nred + 255) / 256), 256, 0, stream>>>(
@@ -708,21 +735,28 @@ cudaError_t launch_bwd_d(const AttnProblem& p, const void* q, const void* k, con
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-#ifndef BLADE_BWD_DQ_MMA_SYNC
-  e = launch_bwd_dq_tc(p, q, k, v, lse, dout, Dvec, kv_idx, kv_cnt, dq, stream, gp);
-  if (e != cudaErrorNotSupported) return e;
-#endif
-  bsa_bwd_dq_kernel<D><<<grid, BW_THREADS, smem_q, stream>>>(
-      B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, kv_idx, kv_cnt,
-      reinterpret_cast<__nv_bfloat16*>(dq));
-  if (gp) {  // + the global tokens' share of dQ (read-modify-write)
-    e = cudaFuncSetAttribute(gt_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if constexpr (!kForceDqMma) {
+    e = launch_bwd_dq_tc(p, q, k, v, lse, dout, Dvec, kv_idx, kv_cnt, dq, stream, gp);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  if constexpr (kBaselines) {
+    e = cudaFuncSetAttribute(bsa_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem_q);
     if (e != cudaSuccess) return e;
-    gt_bwd_dq_kernel<D><<<dim3(unsigned((p.N + BW_ROWS - 1) / BW_ROWS), unsigned(p.BH)),
-                          BW_THREADS, smem_q, stream>>>(
-        B(q), B(gp->kg), B(gp->vg), B(dout), lse, Dvec, p.N, gp->Ng, gp->window, p.scale,
+    bsa_bwd_dq_kernel<D><<<grid, BW_THREADS, smem_q, stream>>>(
+        B(q), B(k), B(v), B(dout), lse, Dvec, p.N, p.Nb, p.scale, kv_idx, kv_cnt,
         reinterpret_cast<__nv_bfloat16*>(dq));
+    if (gp) {  // + the global tokens' share of dQ (read-modify-write)
+      e = cudaFuncSetAttribute(gt_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_q);
+      if (e != cudaSuccess) return e;
+      gt_bwd_dq_kernel<D><<<dim3(unsigned((p.N + BW_ROWS - 1) / BW_ROWS), unsigned(p.BH)),
+                            BW_THREADS, smem_q, stream>>>(
+          B(q), B(gp->kg), B(gp->vg), B(dout), lse, Dvec, p.N, gp->Ng, gp->window, p.scale,
+          reinterpret_cast<__nv_bfloat16*>(dq));
+    }
+  } else {
+    return cudaErrorNotSupported;
   }
   return cudaGetLastError();
 }

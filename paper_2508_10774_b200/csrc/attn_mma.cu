@@ -15,6 +15,7 @@
 #include "internal.h"
 
 namespace blade {
+#ifdef BLADE_WITH_BASELINES  // comparison baseline, not in the product build
 namespace {
 
 constexpr int AM_ROWS = 128;
@@ -202,5 +203,12 @@ cudaError_t launch_attn_mma(const AttnProblem& p, const void* q, const void* k,
   if (p.d == 128) return launch_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, stream);
   return cudaErrorInvalidValue;
 }
+
+#else
+cudaError_t launch_attn_mma(const AttnProblem&, const void*, const void*, const void*,
+                            const int32_t*, const int32_t*, void*, float*, cudaStream_t) {
+  return cudaErrorNotSupported;
+}
+#endif  // BLADE_WITH_BASELINES
 
 }  // namespace blade

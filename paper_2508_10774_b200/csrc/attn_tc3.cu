@@ -27,6 +27,7 @@
 #include "tma_host.h"
 
 namespace blade {
+#ifdef BLADE_WITH_BASELINES  // comparison baseline, not in the product build
 namespace {
 
 using attn::DefaultScale;
@@ -374,5 +375,13 @@ cudaError_t launch_attn_tc3(const AttnProblem& p, const void* q, const void* k, 
   if (p.d == 128) return launch3_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream);
   return cudaErrorNotSupported;
 }
+
+#else
+cudaError_t launch_attn_tc3(const AttnProblem&, const void*, const void*, const void*,
+                            const int32_t*, const int32_t*, void*, float*, cudaStream_t,
+                            const GtProblem*) {
+  return cudaErrorNotSupported;
+}
+#endif  // BLADE_WITH_BASELINES
 
 }  // namespace blade

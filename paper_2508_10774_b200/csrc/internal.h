@@ -32,14 +32,10 @@ struct MaskWorkspace {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// K-mask.2 on the probe2.cu tcgen05 probe (else probe_tc.cu / the mma.sync probe)?
+// K-mask.2 on the probe2.cu tcgen05 probe (else the mma.sync probe)?
 bool probe2_supported(int d, int kk, int Nb, int64_t BH, int N);
 inline bool mask_uses_probe2(const MaskProblem& p) {
-#ifdef BLADE_PROBE_V1  // timing experiment: the round-1 probe on gathered copies
-  return false;
-#else
   return probe2_supported(p.d, p.kk, p.Nb, p.BH, p.N);
-#endif
 }
 
 inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
@@ -68,27 +64,18 @@ cudaError_t launch_mask(const MaskProblem& p, const void* q, const void* k, uint
                         int32_t* sample_idx, int32_t* n_refined, char* ws,
                         cudaStream_t stream);
 
-// Selection fused into the tcgen05 probe's epilogue (K-mask.3).
-struct ProbeSelect {
-  double tau;
-  int lo, hi;
-  double guard;
-  uint8_t* mask;
-  int32_t* kv_idx;
-  int32_t* kv_cnt;
-  int* counters;
-  int32_t* flags;
-  int* done;
-  int neg_flagged;
-};
-
-bool probe_tc_supported(int d, int kk, int Nb);
-bool probe_tc_selects();  // selection fused into the probe epilogue?
 cudaError_t launch_probe2(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
                           const void* qs, const void* ks, float* pimp, cudaStream_t stream);
-cudaError_t launch_probe_tc(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
-                            const void* qs, const void* ks, float* pimp, const ProbeSelect* sel,
-                            cudaStream_t stream);
+// Attention implementations compiled into this library: AUTO / TCGEN05_PAIR
+// (attn_tc2.cu) and TCGEN05 (attn_tc.cu) always; the mma.sync and
+// three-S-buffer kernels only into -DBLADE_WITH_BASELINES builds.
+inline bool impl_built(int impl) {
+#ifdef BLADE_WITH_BASELINES
+  return impl >= 0 && impl <= 4;
+#else
+  return impl == 0 || impl == 1 || impl == 3;
+#endif
+}
 
 struct AttnProblem {
   int64_t BH;

@@ -897,23 +897,14 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         ks, counters);
   }
   if (p2) {
-    // K-mask.2: tcgen05 probe, even / odd tiles on two warp halves (probe2.cu)
+    // K-mask.2: tcgen05 probe (probe2.cu): k in {16, 32, 64}, N_b <= 256
     e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
     if (e != cudaSuccess) return e;
     select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
         pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
         done, p.neg_flagged);
-  } else   if (probe_tc_supported(D, p.kk, p.Nb)) {
-    // K-mask.2 + K-mask.3 fused: tcgen05 probe, selection in its epilogue
-    ProbeSelect ps{p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done,
-                   p.neg_flagged};
-    e = launch_probe_tc(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, &ps, stream);
-    if (e != cudaSuccess) return e;
-    if (!probe_tc_selects())  // K-mask.3 as its own launch (warm instruction cache)
-      select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
-          pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
-          done, p.neg_flagged);
   } else {
+    // k = 128 or N_b > 256: the mma.sync probe (R of a 64-row tile in smem)
     if (p.kk > PR_ROWS) {
       e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);
       if (e != cudaSuccess) return e;

@@ -19,3 +19,4 @@ def cuda_dev():
     if not torch.cuda.is_available():
         pytest.fail("GPU test run without a visible CUDA device")
     return torch.device("cuda:0")
+

@@ -47,7 +47,12 @@ def test_status_strings_and_version(asa):
     lib = asa._lib
     for s in range(5):
         assert lib.blade_status_string(s)
-    assert asa.version() >= 100
+    assert asa.version() >= 200
+    # product build: the pair / one-block tcgen05 kernels only; the mma.sync and
+    # three-S-buffer comparison kernels are -DBLADE_WITH_BASELINES-only
+    assert asa.impl_built(asa.ATTN_AUTO) and asa.impl_built(asa.ATTN_TCGEN05_PAIR)
+    assert asa.impl_built(asa.ATTN_TCGEN05)
+    assert not asa.impl_built(asa.ATTN_MMA_SYNC) and not asa.impl_built(asa.ATTN_TCGEN05_TRIPLE)
 
 
 def test_workspace_sizes(asa):

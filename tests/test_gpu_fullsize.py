@@ -66,13 +66,13 @@ def test_fullsize_mask_and_sampled_attention(A, case):
         PT.check_attention(o[u], lse[u], o_ref, lse_ref)
 
 
-def test_fullsize_mma_baseline_agrees(A):
-    """The mma.sync baseline and the tcgen05 kernel on the Wan layer."""
+def test_fullsize_one_block_kernel_agrees(A):
+    """The one-block tcgen05 kernel and the pair kernel (AUTO) on the Wan layer."""
     q, k, v = _inputs("wan")
     qd, kd, vd = PT.to_dev(q, k, v)
     m = A.blade_asa_mask(qd, kd, tau=0.9, keep_min=51, keep_max=51)
     o1, l1 = A.blade_bsa_fwd(qd, kd, vd, m.kv_idx, m.kv_cnt, impl=A.ATTN_TCGEN05)
-    o2, l2 = A.blade_bsa_fwd(qd, kd, vd, m.kv_idx, m.kv_cnt, impl=A.ATTN_MMA_SYNC)
+    o2, l2 = A.blade_bsa_fwd(qd, kd, vd, m.kv_idx, m.kv_cnt, impl=A.ATTN_AUTO)
     torch.cuda.synchronize()
     assert (o1.float() - o2.float()).abs().max().item() <= 2e-2
     assert (l1 - l2).abs().max().item() <= 1e-3

@@ -17,7 +17,7 @@ def A(cuda_dev):
 
 
 @pytest.mark.parametrize("guard", [0.0, 1e-3, 1e30])
-@pytest.mark.parametrize("d,impl", [(128, 0), (64, 0), (128, 1), (64, 3), (128, 2), (128, 4)])
+@pytest.mark.parametrize("d,impl", [(128, 0), (64, 0), (128, 1), (64, 3), (64, 1)])
 def test_fused_equals_two_calls(A, d, impl, guard):
     q, k, v = inputs.smooth(1, 3, 2000, d, (1, 1, 2000), ell=3.0, beta=9.0, seed=d)
     qd, kd, vd = (t.cuda() for t in (q, k, v))
@@ -58,7 +58,7 @@ def test_fused_edges_lpt(A, N, d):
 
 @pytest.mark.parametrize("guard", [0.0, 1e30])
 @pytest.mark.parametrize("N,d,n,impl", [(2000, 128, 128, 0), (2000, 64, 100, 0), (1407, 128, 7, 1),
-                                        (300, 64, 1000, 3), (2000, 128, 128, 4)])
+                                        (300, 64, 1000, 3), (2000, 64, 128, 1)])
 def test_fused_gt_equals_separate_calls(A, N, d, n, impl, guard):
     """blade_asa_gt_fwd (MeanPool_n + mask + ASA_GT attention, PDL) equals
     blade_gt_pool + blade_asa_mask + blade_bsa_gt_fwd bit for bit; the MMA_SYNC

@@ -22,8 +22,9 @@ def A(cuda_dev):
     return asa
 
 
-IMPLS = [pytest.param(2, id="mma_sync"), pytest.param(1, id="tcgen05"), pytest.param(3, id="pair"),
-         pytest.param(4, id="triple")]
+# the product kernels (AUTO = the pair kernel); the mma.sync and three-S-buffer
+# baselines are compiled only into -DBLADE_WITH_BASELINES builds
+IMPLS = [pytest.param(1, id="tcgen05"), pytest.param(3, id="pair")]
 
 
 def _run_mask(A, q, k, p: O.AsaParams, **kw):
