@@ -589,7 +589,11 @@ def sparse_attention_gt(q, k, v, kv_idx, kv_cnt, b: int, n: int, scale: float | 
 #     wide, else cut it into three parts (one step along the short side, the
 #     long run, one step back), halves rounded so the sub-rectangles' major
 #     sides are even where possible, which is what keeps consecutive cells
-#     adjacent.
+#     adjacent.  This is the published generalised-Hilbert ("gilbert2d")
+#     recursion of J. Cerveny (github.com/jakubcerveny/gilbert, BSD-2-Clause),
+#     the curve the paper names; it is pinned by the curve's
+#     properties (tests/test_oracle_gilbert.py), not by the CUDA side, which
+#     implements the same published recursion.
 # ---------------------------------------------------------------------------
 
 

@@ -17,7 +17,13 @@
 // two halves along a; otherwise it is cut into three: a strip along b of
 // half height (walked with a and b swapped), the remaining wide part, and the
 // return strip walked backwards.  Halves are nudged to even lengths where
-// that keeps consecutive cells adjacent.
+// that keeps consecutive cells adjacent.  This is the published generalised
+// Hilbert ("gilbert2d") recursion of J. Cerveny (github.com/jakubcerveny/
+// gilbert, BSD-2-Clause), the curve the paper names; the oracle
+// (oracle/asa_oracle.py) implements the same published recursion, so the
+// independent pins of both are the curve's properties (exhaustive adjacency,
+// Hilbert quadrant structure, tests/test_oracle_gilbert.py), not their
+// agreement.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

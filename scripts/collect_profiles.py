@@ -3,7 +3,7 @@
 into profiles/ under a round prefix, summarise the ncu reports, and update
 profiles/traffic.json from the full captures.
 
-    python scripts/collect_profiles.py r01
+    python scripts/collect_profiles.py r02
 """
 import csv
 import io
@@ -49,7 +49,15 @@ def main():
               "bench_bwd_cog_asa_gt.json": "bench_bwd_cog_asa_gt.json",
               "launches_wan.csv": "launches_wan_keep51.csv", "launches_cog.csv": "launches_cog_keep25.csv",
               "launches_bwd_wan.csv": "launches_bwd_wan.csv", "sweep_wan.jsonl": "sweep_wan.jsonl",
-              "pytest_gpu.log": "pytest_gpu.log", "smoke.log": "smoke.log"}
+              "pytest_gpu.log": "pytest_gpu.log", "smoke.log": "smoke.log",
+              "bench_wan_200.json": "bench_wan_sustained200.json",
+              "bench_wan_tau.json": "bench_wan_tau0.9.json",
+              "mask_time_wan.jsonl": "mask_time_wan.jsonl", "mask_time_cog.jsonl": "mask_time_cog.jsonl",
+              "pipes_wan.csv": "pipes_wan_keep51.csv", "pipes_cog.csv": "pipes_cog_keep25.csv",
+              "pipes_wan_tau95.csv": "pipes_wan_tau0.95.csv",
+              "sanitizer_memcheck.log": "sanitizer_memcheck.log",
+              "sanitizer_racecheck.log": "sanitizer_racecheck.log",
+              "sanitizer_synccheck.log": "sanitizer_synccheck.log"}
     for s, d in copies.items():
         p = os.path.join(SRC, s)
         if os.path.exists(p):
