@@ -300,10 +300,19 @@ def _ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+def gpu_head_start(stream) -> None:
+    """Keep the GPU busy (~10 ms spin, untimed) while the host enqueues the
+    timed calls, so a host-side stall (Python, the clock sampler starting)
+    cannot open an idle gap inside the timed region."""
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(20_000_000)
+
+
 def time_loop(fn, steps: int, stream) -> float:
     """Mean ms per call of ``steps`` back-to-back calls (CUDA events on the
     launching stream)."""
     e0, e1 = _ev(), _ev()
+    gpu_head_start(stream)
     e0.record(stream)
     for _ in range(steps):
         fn()
@@ -364,6 +373,7 @@ def run_stack(args, ws, rank, local, dev, *, sub: bool = False):
     e0, e1 = _ev(), _ev()
     gstarts = [_ev() for _ in range(args.steps)]
     gends = [_ev() for _ in range(args.steps)]
+    gpu_head_start(stream)
     e0.record(stream)
     for s in range(args.steps):
         ev_g[0] = gstarts[s]
@@ -473,6 +483,7 @@ def measure_layer(args, workload: str, dev, local: int, *, headline: bool):
     starts = [_ev() for _ in range(args.steps)]
     mids = [_ev() for _ in range(args.steps)]
     ends = [_ev() for _ in range(args.steps)]
+    gpu_head_start(stream)
     for s in range(args.steps):
         starts[s].record(stream)
         ev_mid[0] = mids[s]
