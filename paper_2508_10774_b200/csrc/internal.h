@@ -2,6 +2,7 @@
 // C-ABI front end (abi.cu) and the kernel translation units.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -49,7 +50,7 @@ inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   w.off_qs = o;       o = align256(o + gath);
   w.off_ks = o;       o = align256(o + gath);
   w.off_pimp = o;     o = align256(o + rows * p.Nb * 4);
-  w.off_counters = o; o = align256(o + 64);
+  w.off_counters = o; o = align256(o + 64);  // [0] refine queue length
   w.off_flags = o;    o = align256(o + rows * 4);
   w.off_done = o;     o = align256(o + rows * 4);
   w.off_r64 = o;      o = align256(o + rows * p.kk * p.Nb * 8);
@@ -63,6 +64,20 @@ cudaError_t launch_mask(const MaskProblem& p, const void* q, const void* k, uint
                         int32_t* kv_idx, int32_t* kv_cnt, float* p_imp_out,
                         int32_t* sample_idx, int32_t* n_refined, char* ws,
                         cudaStream_t stream);
+
+// K-mask.2-3 as one persistent kernel (mask_fused.cu), a programmatic dependent
+// of K-mask.1: k in {16, 32, 64}, N_b <= 256.
+struct MaskFusedBufs {
+  __nv_bfloat16* qs;
+  __nv_bfloat16* ks;
+  int* counters;
+  int32_t* flags;
+  int* done;
+};
+bool mask_fused_supported(const MaskProblem& p);
+cudaError_t launch_mask_fused(const MaskProblem& p, uint8_t* mask, int32_t* kv_idx,
+                              int32_t* kv_cnt, float* p_imp_out, const MaskFusedBufs& w,
+                              cudaStream_t stream);
 
 cudaError_t launch_probe2(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
                           const void* qs, const void* ks, float* pimp, cudaStream_t stream);

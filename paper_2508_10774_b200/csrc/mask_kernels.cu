@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
   __shared__ int cand_o[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * 8 + warp;
+  // the fused probe/select kernel (a programmatic dependent) may be scheduled
+  // now; it waits for this grid's completion before reading Q_s / K_s
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (w == 0 && lane == 0) counters[0] = 0;  // refine queue length
   const bool active = w < BH * Nb * 2;
   const int which = int(w & 1);
@@ -783,51 +786,38 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
     __syncthreads();
     if (!last) continue;
     __threadfence();
-    // l.14 combine, spread over all threads: (query row q, chunk stripe z);
-    // each thread issues all of its loads before using any (one L2 latency)
+    // l.14 combine in one pass, spread over all threads: (query row q, chunk
+    // stripe z) merges its chunks' (M_c, l_c) online, then the 8 stripes of a
+    // row are merged through shared memory
     for (int qg = 0; qg < ki; qg += 16) {  // query rows in groups of 16
       const int q = qg + (tid & 15), z = tid >> 4;  // 16 rows x 8 stripes
-      constexpr int kMaxPer = 16;            // loads in flight per thread and pass
-      double M = -INFINITY;
-      for (int b0 = 0; b0 < nchunks; b0 += 8 * kMaxPer) {
-        double mv[kMaxPer];
-#pragma unroll
-        for (int e = 0; e < kMaxPer; ++e) {
-          const int cc = b0 + z + 8 * e;
-          const bool ok = q < ki && cc < nchunks;
-          mv[e] = ok ? __ldcg(&mpart[(int64_t(f) * nchunks + cc) * kk + q]) : -INFINITY;
+      double M = -INFINITY, l = 0.0;
+      for (int cc = z; cc < nchunks; cc += 8) {
+        const bool ok = q < ki;
+        const int64_t o = (int64_t(f) * nchunks + cc) * kk + (ok ? q : 0);
+        const double mc = ok ? __ldcg(&mpart[o]) : -INFINITY;
+        const double lc = ok ? __ldcg(&lpart[o]) : 0.0;
+        if (mc == -INFINITY) continue;
+        if (mc > M) {
+          l = l * exp(M - mc) + lc;  // exp(-inf) = 0 on the first chunk
+          M = mc;
+        } else {
+          l += lc * exp(mc - M);
         }
-#pragma unroll
-        for (int e = 0; e < kMaxPer; ++e) M = fmax(M, mv[e]);
       }
       sRg[z][q - qg] = M;
       __syncthreads();
-      M = sRg[0][q - qg];
+      double Mt = sRg[0][q - qg];
 #pragma unroll
-      for (int zz = 1; zz < 8; ++zz) M = fmax(M, sRg[zz][q - qg]);
-      double l = 0.0;
-      for (int b0 = 0; b0 < nchunks; b0 += 8 * kMaxPer) {
-        double mv[kMaxPer], lv[kMaxPer];
-#pragma unroll
-        for (int e = 0; e < kMaxPer; ++e) {
-          const int cc = b0 + z + 8 * e;
-          const bool ok = q < ki && cc < nchunks;
-          const int64_t o = (int64_t(f) * nchunks + (ok ? cc : 0)) * kk + (ok ? q : 0);
-          mv[e] = ok ? __ldcg(&mpart[o]) : -INFINITY;
-          lv[e] = ok ? __ldcg(&lpart[o]) : 0.0;
-        }
-#pragma unroll
-        for (int e = 0; e < kMaxPer; ++e)
-          if (mv[e] != -INFINITY) l += lv[e] * exp(mv[e] - M);
-      }
+      for (int zz = 1; zz < 8; ++zz) Mt = fmax(Mt, sRg[zz][q - qg]);
       __syncthreads();
-      sRg[z][q - qg] = l;
+      sRg[z][q - qg] = M == -INFINITY ? 0.0 : l * exp(M - Mt);
       __syncthreads();
       if (z == 0 && q < ki) {
         double lt = 0.0;
 #pragma unroll
         for (int zz = 0; zz < 8; ++zz) lt += sRg[zz][q - qg];
-        sMs[q] = M + log(lt);  // P~ = e^{L - M} / l = e^{L - (M + ln l)}
+        sMs[q] = Mt + log(lt);  // P~ = e^{L - M} / l = e^{L - (M + ln l)}
       }
       __syncthreads();
     }
@@ -851,10 +841,18 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
 #ifdef BLADE_RF_TIMING
     const unsigned long long t_sel = gtime();
 #endif
-    // l.7-10 in fp64 by the whole CTA (shared-memory bitonic sort)
-    cta_select_f64<RF_THREADS>(sRow, Nb, tau, lo, hi, mask ? mask + row * Nb : nullptr,
-                               kv_idx + row * Nb, kv_cnt + row,
-                               reinterpret_cast<char*>(sRow + kMaxNb));
+    // l.7-10 in fp64 by one warp (register bitonic sort of the fp64 row,
+    // select.cuh); the CTA-wide shared-memory sort (cta_select_f64) took
+    // ~14 us per row, serialised on the row's last chunk
+    if (Nb <= 256) {
+      if (warp == 0)
+        select_row(sRow, Nb, tau, lo, hi, 0.0, false, mask ? mask + row * Nb : nullptr,
+                   kv_idx + row * Nb, kv_cnt + row, reinterpret_cast<uint32_t*>(sRow + kMaxNb));
+    } else {
+      cta_select_f64<RF_THREADS>(sRow, Nb, tau, lo, hi, mask ? mask + row * Nb : nullptr,
+                                 kv_idx + row * Nb, kv_cnt + row,
+                                 reinterpret_cast<char*>(sRow + kMaxNb));
+    }
 #ifdef BLADE_RF_TIMING
     if (tid == 0) {
       const unsigned long long t_done = gtime();
@@ -896,7 +894,13 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
         ks, counters);
   }
-  if (p2) {
+  if (mask_fused_supported(p)) {
+    // K-mask.2-3 in one persistent kernel (mask_fused.cu), a programmatic
+    // dependent of K-mask.1
+    e = launch_mask_fused(p, mask, kv_idx, kv_cnt, p_imp_out,
+                          MaskFusedBufs{qs, ks, counters, flags, done}, stream);
+    if (e != cudaSuccess) return e;
+  } else if (p2) {
     // K-mask.2: tcgen05 probe (probe2.cu): k in {16, 32, 64}, N_b <= 256
     e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
     if (e != cudaSuccess) return e;

@@ -39,6 +39,7 @@ for cfg in args.configs.split(","):
     ts = []
     for _ in range(args.steps):
         flush.zero_()
+        torch.cuda._sleep(2_000_000)  # GPU busy while the host enqueues the timed call
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         m = A.blade_asa_mask(q, k, want_mask=False, **kw)
