@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     }
   } else if (warp == kWMma) {
     // ===================== MMA issuer =====================
-    if (lane == 0 && total > 0) {
+    if (BLADE_ISSUER(lane) && total > 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idQ = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t qa = smem_u32(sQ), da = smem_u32(sDO);
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-          tc::mma_ss(tmem + d_col, tc::sw128_desc(a + off, 16, 1024),
+          BLADE_MMA_SS(tmem + d_col, tc::sw128_desc(a + off, 16, 1024),
                      tc::sw128_desc(b + off, 16, 1024), idS, ks > 0);
         }
       };
@@ -201,15 +201,15 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
         tc::mbar_wait(bar_kfull + s, (n / C::kRingK) & 1);
         tc::fence_after_sync();
         ss(C::kColS, qa, kbase + s * C::kTile);
-        tc::commit(bar_sc);
+        BLADE_COMMIT(bar_sc);
       };
       auto issue_dP = [&](int n) {
         const int s = n % C::kRingV;
         tc::mbar_wait(bar_vfull + s, (n / C::kRingV) & 1);
         tc::fence_after_sync();
         ss(C::kColDP, da, vbase + s * C::kTile);
-        tc::commit(bar_dp);
-        tc::commit(bar_vempty + s);
+        BLADE_COMMIT(bar_dp);
+        BLADE_COMMIT(bar_vempty + s);
       };
       issue_S(0);
       issue_dP(0);
@@ -223,13 +223,13 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
         const uint32_t kb = kbase + (n % C::kRingK) * C::kTile;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          tc::mma_ts(tmem + C::kColDQ, tmem + kColDS + ks * 8,
+          BLADE_MMA_TS(tmem + C::kColDQ, tmem + kColDS + ks * 8,
                      tc::sw128_desc(kb + ks * 2048, C::kPanel, 1024), idQ,
                      (n > 0 || ks > 0) ? 1 : 0);
         // only the last dQ MMA is awaited (tcgen05 ops of one thread complete
         // in order): one commit, one phase, every phase has a waiter
-        if (n + 1 == total) tc::commit(bar_dq);
-        tc::commit(bar_kempty + (n % C::kRingK));
+        if (n + 1 == total) BLADE_COMMIT(bar_dq);
+        BLADE_COMMIT(bar_kempty + (n % C::kRingK));
         if (n + 1 < total) issue_dP(n + 1);
       }
       tc::mbar_wait(bar_dq, 0);
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
     }
   } else if (warp == kWMma) {
     // ===================== MMA issuer =====================
-    if (lane == 0 && cnt > 0) {
+    if (BLADE_ISSUER(lane) && cnt > 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idG = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t ka = smem_u32(sK), va = smem_u32(sV), rb = smem_u32(sRing);
@@ -463,14 +463,14 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-          tc::mma_ss(tmem + d_col, tc::sw128_desc(a + off, 16, 1024),
+          BLADE_MMA_SS(tmem + d_col, tc::sw128_desc(a + off, 16, 1024),
                      tc::sw128_desc(b + off, 16, 1024), idS, ks > 0);
         }
       };
       auto ts = [&](uint32_t d_col, uint32_t a_col, uint32_t b, bool acc) {  // D += A(TMEM) B
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          tc::mma_ts(tmem + d_col, tmem + a_col + ks * 8,
+          BLADE_MMA_TS(tmem + d_col, tmem + a_col + ks * 8,
                      tc::sw128_desc(b + ks * 2048, C::kPanel, 1024), idG, (acc || ks > 0) ? 1 : 0);
       };
       auto slot_q = [&](int n) { return rb + (n % C::kRing) * 2 * C::kTile; };
@@ -480,9 +480,9 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
       };
       wait_full(0);
       ss(C::kColS, ka, slot_q(0));                 // S^T(0)
-      tc::commit(bar_sc);
+      BLADE_COMMIT(bar_sc);
       ss(C::kColDP, va, slot_q(0) + C::kTile);     // dP^T(0)
-      tc::commit(bar_dp);
+      BLADE_COMMIT(bar_dp);
       for (int n = 0; n < cnt; ++n) {
         tc::mbar_wait(bar_p, n & 1);
         tc::fence_after_sync();
@@ -490,16 +490,16 @@ __global__ void __launch_bounds__(bwd_threads<EWG>(), 1)
         if (n + 1 < cnt) {
           wait_full(n + 1);
           ss(C::kColS, ka, slot_q(n + 1));         // S^T(n+1) (after dV(n) read P^T(n))
-          tc::commit(bar_sc);
+          BLADE_COMMIT(bar_sc);
         }
         tc::mbar_wait(bar_ds, n & 1);
         tc::fence_after_sync();
         ts(C::kColDK, kColDSt, slot_q(n), n > 0);  // dK += dS^T Q_i
-        if (n + 1 == cnt) tc::commit(bar_dk);  // only the last is awaited (see bar_dq)
-        tc::commit(bar_empty + (n % C::kRing));
+        if (n + 1 == cnt) BLADE_COMMIT(bar_dk);  // only the last is awaited (see bar_dq)
+        BLADE_COMMIT(bar_empty + (n % C::kRing));
         if (n + 1 < cnt) {
           ss(C::kColDP, va, slot_q(n + 1) + C::kTile);  // dP^T(n+1) (after dK(n) read dS^T(n))
-          tc::commit(bar_dp);
+          BLADE_COMMIT(bar_dp);
         }
       }
       tc::mbar_wait(bar_dk, 0);

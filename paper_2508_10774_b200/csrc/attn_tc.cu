@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
+    if (BLADE_ISSUER(lane)) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
@@ -288,11 +288,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           // A = Q from TMEM (16 d-values = 8 columns per k-step): the tensor core
           // then reads only K from shared memory, which keeps the S MMA off the
           // smem-bandwidth limit
-          tc::mma_ts(tmem + buf * 128, tmem + C::kColQ + ks * 8, tc::sw128_desc(kb + off, 16, 1024),
+          BLADE_MMA_TS(tmem + buf * 128, tmem + C::kColQ + ks * 8, tc::sw128_desc(kb + off, 16, 1024),
                      idS, ks > 0);
         }
-        tc::commit(bar_s + buf);
-        tc::commit(bar_kempty + s);
+        BLADE_COMMIT(bar_s + buf);
+        BLADE_COMMIT(bar_kempty + s);
       };
       TC_DBG(1, 1);
       tc::mbar_wait(bar_qt, 0);
@@ -317,12 +317,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef BLADE_ATTN_SKIP_PV  // timing experiment only
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          tc::mma_ts(tmem + C::kColO, tmem + buf * 128 + 64 + ks * 8,
+          BLADE_MMA_TS(tmem + C::kColO, tmem + buf * 128 + 64 + ks * 8,
                      tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                      (n > 0 || ks > 0) ? 1 : 0);
 #endif
-        tc::commit(bar_pv);
-        tc::commit(bar_vempty + s);
+        BLADE_COMMIT(bar_pv);
+        BLADE_COMMIT(bar_vempty + s);
         if (n + 2 < cnt) issue_S(n + 2);
       }
       // drain: the last commits must land before the CTA's smem is released

@@ -72,8 +72,8 @@ struct Cfg2 {
   static constexpr int kOffRingK = 2 * kTile;
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
   static constexpr int kOffBar = kOffRingV + kRingV * kTile;
-  // bar_q, kfull/kempty, vfull/vempty, per block: s, p, pv, sf, sl, slf, 3 P chunks
-  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 9 * 2;
+  // bar_q, kfull/kempty, vfull/vempty, per block: s, p, pv, sf, sl, slf
+  static constexpr int kNumBar = 1 + 2 * kRingK + 2 * kRingV + 6 * 2;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;
   static constexpr int kSmem = kOffMisc + 16 + 1024;  // + alignment slack
   static constexpr uint32_t kColO = 256;
@@ -102,19 +102,6 @@ struct Cfg2 {
 #define BLADE_ATTN2_HALF_S 0
 #endif
   static constexpr bool kHalfS = BLADE_ATTN2_HALF_S && !kSepP;
-  // Option: P handed to the tensor core in kPChunks key chunks (the softmax
-  // signals each stored chunk, the issuer starts that chunk's P V MMAs).
-  // Parity green but no faster (Wan 1.19-1.27 / Cog 1.087 ms with 4 chunks
-  // vs 1.19-1.22 / 1.031 with 1, 2 chunks 1.21-1.24 / 1.030; interleaved on
-  // one box): the single issuer thread blocks at the tensor pipe's pace, so
-  // a chunk's MMAs cannot be issued before the other block's S MMAs ahead of
-  // them in program order have drained, and the extra tcgen05.wait::st per
-  // chunk lengthens the softmax (trace: period 3556 vs 3300 cycles per item).
-#ifndef BLADE_ATTN2_PCHUNKS
-#define BLADE_ATTN2_PCHUNKS 1
-#endif
-  static constexpr int kPChunks = (kHalfS || kSepP) ? 1 : BLADE_ATTN2_PCHUNKS;
-  static_assert(kPChunks == 1 || kPChunks == 2 || kPChunks == 4, "P chunks");
 };
 
 constexpr int kThreads2 = 384;
@@ -181,7 +168,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint64_t* bar_sf = bar_pv + 2;             // [2] S of block t read out (kSepP, 4 warps)
   uint64_t* bar_sl = bar_sf + 2;             // [2] late half of S computed (kHalfS)
   uint64_t* bar_slf = bar_sl + 2;            // [2] late half of S read out (kHalfS, 4 warps)
-  uint64_t* bar_pc = bar_slf + 2;            // [2][3] P chunk c of block t stored (4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -225,7 +211,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::mbar_init(bar_sf + t, 4);
       tc::mbar_init(bar_sl + t, 1);
       tc::mbar_init(bar_slf + t, 4);
-      for (int c = 0; c < 3; ++c) tc::mbar_init(bar_pc + t * 3 + c, 4);
     }
     tc::fence_barrier_init();
   }
@@ -292,7 +277,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
   } else if (warp == 8) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
+    if (BLADE_ISSUER(lane)) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, D, 0, 1);
       const uint32_t qbase = smem_u32(sQ), kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
@@ -308,40 +293,34 @@ __global__ void __launch_bounds__(kThreads2, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-          tc::mma_ss(tmem + t * 128, tc::sw128_desc(qb + off, 16, 1024),
+          BLADE_MMA_SS(tmem + t * 128, tc::sw128_desc(qb + off, 16, 1024),
                      tc::sw128_desc(kb + off, 16, 1024), idS, ks > 0);
         }
-        tc::commit(bar_s + t);
-        tc::commit(bar_kempty + s);
+        BLADE_COMMIT(bar_s + t);
+        BLADE_COMMIT(bar_kempty + s);
         ++gk;
       };
       auto issue_PV = [&](int t, int k) {  // O_t += P_t V of block t's item k
         const int s = gv % C::kRingV;
         tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
         TR2(8 + t, k);
+        tc::mbar_wait(bar_p + t, k & 1);
+        tc::fence_after_sync();
+        TR2(4 + t, k);
         const uint32_t vb = vbase + s * C::kTile;
         const uint32_t pcol = C::kSepP ? C::kColP + t * 64 : t * 128 + 64;
-        constexpr int kPer = 8 / C::kPChunks;  // K = 16 MMAs per P chunk
 #pragma unroll
-        for (int pc = 0; pc < C::kPChunks; ++pc) {
-          tc::mbar_wait(pc + 1 < C::kPChunks ? bar_pc + t * 3 + pc : bar_p + t, k & 1);
-          tc::fence_after_sync();
-          if (pc + 1 == C::kPChunks) TR2(4 + t, k);
-#pragma unroll
-          for (int kq = 0; kq < kPer; ++kq) {
-            const int ks = pc * kPer + kq;
-            tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
-                       tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
-                       (k > 0 || ks > 0) ? 1 : 0);
-          }
-        }
+        for (int ks = 0; ks < 8; ++ks)
+          BLADE_MMA_TS(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
+                     tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
+                     (k > 0 || ks > 0) ? 1 : 0);
         // bar_pv: with kSepP the softmax waits for every P V; otherwise only
         // the last one is awaited (S(n) is issued after P V(n-1), and tcgen05
         // ops of one thread complete in order), so only the last is committed
         // and every phase of the barrier has a waiter (compute-sanitizer
         // synccheck flags a phase nobody waits for)
-        if (C::kSepP || k + 1 == (t ? cnt1 : cnt0)) tc::commit(bar_pv + t);
-        tc::commit(bar_vempty + s);
+        if (C::kSepP || k + 1 == (t ? cnt1 : cnt0)) BLADE_COMMIT(bar_pv + t);
+        BLADE_COMMIT(bar_vempty + s);
         ++gv;
       };
       if constexpr (C::kHalfS) {
@@ -362,11 +341,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
             const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-            tc::mma_ss(tmem + dst, tc::sw128_desc(qb + off, 16, 1024),
+            BLADE_MMA_SS(tmem + dst, tc::sw128_desc(qb + off, 16, 1024),
                        tc::sw128_desc(kb + off, 16, 1024), idS64, ks > 0);
           }
-          tc::commit(h ? bar_sl + t : bar_s + t);
-          if (h) tc::commit(bar_kempty + s);
+          BLADE_COMMIT(h ? bar_sl + t : bar_s + t);
+          if (h) BLADE_COMMIT(bar_kempty + s);
         };
         auto issue_PVh = [&](int t, int k) {  // O_t += P_t(k) V, P_t(k) in E_k
           const int s = gv % C::kRingV;
@@ -377,11 +356,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
           const uint32_t pcol = t * 128 + (k & 1) * 64;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
-            tc::mma_ts(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
+            BLADE_MMA_TS(tmem + C::kColO + t * D, tmem + pcol + ks * 8,
                        tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                        (k > 0 || ks > 0) ? 1 : 0);
-          tc::commit(bar_pv + t);
-          tc::commit(bar_vempty + s);
+          BLADE_COMMIT(bar_pv + t);
+          BLADE_COMMIT(bar_vempty + s);
           ++gv;
         };
         for (int t = 0; t < 2; ++t)
@@ -590,8 +569,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0 && C::kSepP) tc::mbar_arrive(bar_sf + t);
-      if (lane == 0)
-        for (int pc = 0; pc + 1 < C::kPChunks; ++pc) tc::mbar_arrive(bar_pc + t * 3 + pc);
       if (lane == 0) tc::mbar_arrive(bar_p + t);
       continue;
 #endif
@@ -682,15 +659,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
         tc::st_32x32b_x16(C::kSepP ? tmem + lane_base + C::kColP + t * 64 + c * 16
                                    : tS + 64 + c * 16,
                           pk);
-        if constexpr (C::kPChunks > 1) {
-          constexpr int kPerC = 4 / C::kPChunks;  // 32-key column groups per P chunk
-          if ((c + 1) % kPerC == 0 && c < 3) {    // chunk stored: its P V may start
-            tc::wait_st();
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(bar_pc + t * 3 + c / kPerC);
-          }
-        }
       }
       const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
       l_sum += acc.x + acc.y;
@@ -811,6 +779,19 @@ cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, 
   if (p.d == 128)
     return launch2_d<128>(p, q, k, v, kv_idx, kv_cnt, o, lse, gt, stream, pdl, order);
   return cudaErrorNotSupported;
+}
+
+cudaError_t launch_attn_auto(const AttnProblem& p, const void* q, const void* k, const void* v,
+                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
+                             cudaStream_t stream, const GtProblem* gt, bool pdl,
+                             const int32_t* order) {
+#ifndef BLADE_ATTN2S_OFF  // d = 64: pair CTAs, column-split softmax (attn_tc2s.cu)
+  if (p.d == 64) return launch_attn_tc2s(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
+#endif
+#ifndef BLADE_ATTN1S_OFF  // d = 128: one block per CTA, split softmax (attn_tc1s.cu)
+  if (p.d == 128) return launch_attn_tc1s(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
+#endif
+  return launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
 }
 
 }  // namespace blade

@@ -104,9 +104,6 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
   __shared__ int cand_o[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * 8 + warp;
-  // the fused probe/select kernel (a programmatic dependent) may be scheduled
-  // now; it waits for this grid's completion before reading Q_s / K_s
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (w == 0 && lane == 0) counters[0] = 0;  // refine queue length
   const bool active = w < BH * Nb * 2;
   const int which = int(w & 1);
@@ -595,7 +592,10 @@ BLADE_DEVINL double bf16_lo_f64(uint32_t w) { return bf16bits_f64(w & 0xffffu); 
 BLADE_DEVINL double bf16_hi_f64(uint32_t w) { return bf16bits_f64(w >> 16); }
 
 template <int D>
-__global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
+#ifndef BLADE_RF_MINB
+#define BLADE_RF_MINB 5  // refine CTAs per SM: tau 0.95 (129 rows) 0.365 ms mask vs 0.452 at 3, 0.386 at 4
+#endif
+__global__ void __launch_bounds__(RF_THREADS, BLADE_RF_MINB) refine_kernel(
     const __nv_bfloat16* __restrict__ qs, const __nv_bfloat16* __restrict__ ks, int N, int Nb,
     int b, int kk, double scale, int nchunks, double tau, int lo, int hi,
     const int* __restrict__ counters, const int32_t* __restrict__ flags, int* __restrict__ done,
@@ -841,18 +841,11 @@ __global__ void __launch_bounds__(RF_THREADS, 3) refine_kernel(
 #ifdef BLADE_RF_TIMING
     const unsigned long long t_sel = gtime();
 #endif
-    // l.7-10 in fp64 by one warp (register bitonic sort of the fp64 row,
-    // select.cuh); the CTA-wide shared-memory sort (cta_select_f64) took
-    // ~14 us per row, serialised on the row's last chunk
-    if (Nb <= 256) {
-      if (warp == 0)
-        select_row(sRow, Nb, tau, lo, hi, 0.0, false, mask ? mask + row * Nb : nullptr,
-                   kv_idx + row * Nb, kv_cnt + row, reinterpret_cast<uint32_t*>(sRow + kMaxNb));
-    } else {
-      cta_select_f64<RF_THREADS>(sRow, Nb, tau, lo, hi, mask ? mask + row * Nb : nullptr,
-                                 kv_idx + row * Nb, kv_cnt + row,
-                                 reinterpret_cast<char*>(sRow + kMaxNb));
-    }
+    // l.7-10 in fp64 by the whole CTA (shared-memory bitonic sort; a warp-level
+    // register sort of the fp64 row measured slower: 38-45 vs 14 us per row)
+    cta_select_f64<RF_THREADS>(sRow, Nb, tau, lo, hi, mask ? mask + row * Nb : nullptr,
+                               kv_idx + row * Nb, kv_cnt + row,
+                               reinterpret_cast<char*>(sRow + kMaxNb));
 #ifdef BLADE_RF_TIMING
     if (tid == 0) {
       const unsigned long long t_done = gtime();
@@ -894,13 +887,7 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
         ks, counters);
   }
-  if (mask_fused_supported(p)) {
-    // K-mask.2-3 in one persistent kernel (mask_fused.cu), a programmatic
-    // dependent of K-mask.1
-    e = launch_mask_fused(p, mask, kv_idx, kv_cnt, p_imp_out,
-                          MaskFusedBufs{qs, ks, counters, flags, done}, stream);
-    if (e != cudaSuccess) return e;
-  } else if (p2) {
+  if (p2) {
     // K-mask.2: tcgen05 probe (probe2.cu): k in {16, 32, 64}, N_b <= 256
     e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
     if (e != cudaSuccess) return e;
@@ -932,7 +919,7 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     if (e != cudaSuccess) return e;
   }
   // K-mask.4 (persistent grid; the queue length is read on the device)
-  refine_kernel<D><<<148 * 3, RF_THREADS, 0, stream>>>(
+  refine_kernel<D><<<148 * BLADE_RF_MINB, RF_THREADS, 0, stream>>>(
       qs, ks, p.N, p.Nb, p.b, p.kk, double(p.scale), w.nchunks, p.tau, p.lo, p.hi, counters,
       flags, done, r64, mpart, lpart, p_imp_out, mask, kv_idx, kv_cnt, n_refined);
 #ifdef BLADE_RF_TIMING

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kP2Threads, 1)
     }
   } else if (warp == kWarpMma2) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
+    if (BLADE_ISSUER(lane)) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
       const uint32_t qa = smem_u32(sQ), rb = smem_u32(sRing);
       tc::mbar_wait(bar_q, 0);
@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(kP2Threads, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * C::kPanel + (ks & 3) * 32;
-          tc::mma_ss(tmem + bsel * 128, tc::sw128_desc(qa + off, 16, 1024),
+          BLADE_MMA_SS(tmem + bsel * 128, tc::sw128_desc(qa + off, 16, 1024),
                      tc::sw128_desc(kb + off, 16, 1024), idS, ks > 0);
         }
-        tc::commit(bar_s + bsel);
-        tc::commit(bar_empty + s);
+        BLADE_COMMIT(bar_s + bsel);
+        BLADE_COMMIT(bar_empty + s);
       }
     }
   } else {

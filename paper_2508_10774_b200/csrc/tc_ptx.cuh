@@ -116,6 +116,46 @@ BLADE_DEVINL void commit(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
+// Warp-collective forms: the WHOLE warp runs the issue loop (warp-uniform
+// control flow, so descriptors and counters live in uniform registers) and
+// one elected lane issues.  The lane-0-only form made the compiler wrap every
+// tcgen05.mma in an ELECT / BRA.U.ANY loop with R2UR moves.
+BLADE_DEVINL void mma_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+BLADE_DEVINL void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+BLADE_DEVINL void commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+#ifndef BLADE_MMA_WARP
+#define BLADE_MMA_WARP 1  // A/B switch: 0 = lane-0 issue loops
+#endif
+#if BLADE_MMA_WARP
+#define BLADE_ISSUER(lane) true
+#define BLADE_MMA_SS tc::mma_ss_w
+#define BLADE_MMA_TS tc::mma_ts_w
+#define BLADE_COMMIT tc::commit_w
+#else
+#define BLADE_ISSUER(lane) ((lane) == 0)
+#define BLADE_MMA_SS tc::mma_ss
+#define BLADE_MMA_TS tc::mma_ts
+#define BLADE_COMMIT tc::commit
+#endif
+
 BLADE_DEVINL void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 BLADE_DEVINL void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
