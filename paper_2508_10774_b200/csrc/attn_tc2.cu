@@ -781,17 +781,4 @@ cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, 
   return cudaErrorNotSupported;
 }
 
-cudaError_t launch_attn_auto(const AttnProblem& p, const void* q, const void* k, const void* v,
-                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                             cudaStream_t stream, const GtProblem* gt, bool pdl,
-                             const int32_t* order) {
-#ifndef BLADE_ATTN2S_OFF  // d = 64: pair CTAs, column-split softmax (attn_tc2s.cu)
-  if (p.d == 64) return launch_attn_tc2s(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
-#endif
-#ifndef BLADE_ATTN1S_OFF  // d = 128: one block per CTA, split softmax (attn_tc1s.cu)
-  if (p.d == 128) return launch_attn_tc1s(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
-#endif
-  return launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
-}
-
 }  // namespace blade

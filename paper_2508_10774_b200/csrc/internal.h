@@ -110,34 +110,6 @@ cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, 
                             cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
                             const int32_t* order = nullptr);
 
-// d = 64: two query blocks per CTA with each block's softmax split over two
-// column halves, each with its own O accumulator (attn_tc2s.cu).
-cudaError_t launch_attn_tc2s(const AttnProblem& p, const void* q, const void* k, const void* v,
-                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                             cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
-                             const int32_t* order = nullptr);
-
-// d = 128: one query block per CTA, S double-buffered, the softmax split over
-// two column halves with one O accumulator each (attn_tc1s.cu).
-cudaError_t launch_attn_tc1s(const AttnProblem& p, const void* q, const void* k, const void* v,
-                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                             cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
-                             const int32_t* order = nullptr);
-// BLADE_ATTN_AUTO: the product kernel per head dim (attn_tc2.cu dispatch).
-cudaError_t launch_attn_auto(const AttnProblem& p, const void* q, const void* k, const void* v,
-                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
-                             cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
-                             const int32_t* order = nullptr);
-// Does the AUTO attention for head dim d run one CTA per PAIR of query blocks
-// (the LPT order is then over pairs)?
-inline bool attn_auto_pairs(int d) {
-#ifndef BLADE_ATTN1S_OFF
-  if (d == 128) return false;  // attn_tc1s: one block per CTA
-#endif
-  (void)d;
-  return true;
-}
-
 // Longest-processing-time order of the attention CTAs (one query block, or a
 // pair of blocks when pairs != 0) by kept-block count, descending; counts may
 // be provisional (negative: -1 - m).  order: [BH * ceil(Nb / (pairs ? 2 : 1))].
