@@ -301,11 +301,12 @@ def _ev():
 
 
 def gpu_head_start(stream) -> None:
-    """Keep the GPU busy (~10 ms spin, untimed) while the host enqueues the
-    timed calls, so a host-side stall (Python, the clock sampler starting)
-    cannot open an idle gap inside the timed region."""
+    """Keep the GPU busy (~200 ms spin, untimed) while the host enqueues the
+    timed calls, so a host-side stall (Python GC, an allocator call, the clock
+    sampler) cannot open an idle gap inside the timed region: a 10 ms spin
+    still let one 56 ms host stall into a two-call step on the B200."""
     with torch.cuda.stream(stream):
-        torch.cuda._sleep(20_000_000)
+        torch.cuda._sleep(400_000_000)
 
 
 def time_loop(fn, steps: int, stream) -> float:

@@ -33,11 +33,8 @@ struct MaskWorkspace {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// K-mask.2 on the probe2.cu tcgen05 probe (else the mma.sync probe)?
+// K-mask.2 (probe2.cu, tcgen05): k in {16, 32, 64, 128}, N_b <= 512.
 bool probe2_supported(int d, int kk, int Nb, int64_t BH, int N);
-inline bool mask_uses_probe2(const MaskProblem& p) {
-  return probe2_supported(p.d, p.kk, p.Nb, p.BH, p.N);
-}
 
 inline MaskWorkspace mask_workspace_layout(const MaskProblem& p) {
   MaskWorkspace w{};

@@ -4,15 +4,15 @@
 //   K-mask.1 sample_gather_kernel  A1-A3: per (unit, block, Q|K) one warp
 //            draws the k_i in-block offsets (counter hash, reading R-1),
 //            and copies the sampled rows, block-major, into Q_s / K_s.
-//   K-mask.2 probe_kernel          A4-A6: per (unit, 64 sampled query rows)
-//            S = Q_s K_s^T on tensor cores, streaming row max M / row sum l
-//            over all N_k sampled keys, the per-(row, key-block) max R, then
-//            P_imp[i, j] = max_{s in block i} e^{R_sj - M_s} / l_s (Alg. 3).
+//   K-mask.2 probe2_kernel (probe2.cu) A4-A6: per (unit, 128 sampled query
+//            rows) S = Q_s K_s^T on the tcgen05 tensor cores, streaming row
+//            max M / row sum l over all N_k sampled keys, the per-(row,
+//            key-block) max R in TMEM, then P_imp[i, j] = max_{s in block i}
+//            e^{R_sj - M_s} / l_s (Alg. 3).
 //   K-mask.3 selection (select.cuh)    A7-A8: one warp per (unit, q-block)
 //            row: fp64 normalisation, register bitonic sort (p desc, id
 //            asc), warp scan, cut at tau, clamp, compaction to kv_idx /
-//            kv_cnt / mask.  Runs in the tcgen05 probe's epilogue (or as
-//            select_kernel after the mma.sync fallback probe).  Rows whose
+//            kv_cnt / mask (select_kernel).  Rows whose
 //            decision margin is inside the guard band of the fp32 probe
 //            error are queued for K-mask.4.
 //   K-mask.4 refine_kernel         the queued rows' P_imp recomputed in fp64
@@ -225,171 +225,7 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K-mask.2  probe (tensor cores via mma.sync m16n8k16; 4 warps x 16 rows)
-// ---------------------------------------------------------------------------
-constexpr int PR_ROWS = 64;   // sampled query rows per CTA
-constexpr int PR_KEYS = 64;   // sampled keys per pipeline stage
-
-template <int D>
-__global__ void __launch_bounds__(128) probe_kernel(const __nv_bfloat16* __restrict__ qs,
-                                                     const __nv_bfloat16* __restrict__ ks,
-                                                     int N, int Nb, int b, int kk,
-                                                     float scale_log2,
-                                                     float* __restrict__ pimp) {
-  extern __shared__ __align__(128) char smem[];
-  char* sQ = smem;                                      // [64][D] bf16 swizzled
-  char* sK = sQ + PR_ROWS * D * 2;                      // [2][64][D]
-  float* sR = reinterpret_cast<float*>(sK + 2 * PR_KEYS * D * 2);  // [64][Nb]
-  float* sM = sR + PR_ROWS * Nb;                        // [64]
-  float* sL = sM + PR_ROWS;                             // [64]
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t u = blockIdx.y;
-  const int NK = Nb * kk;
-  const int row0 = blockIdx.x * PR_ROWS;
-  const __nv_bfloat16* gQ = qs + u * int64_t(NK) * D;
-  const __nv_bfloat16* gK = ks + u * int64_t(NK) * D;
-  constexpr int CH = D / 8;
-
-  // Q tile
-  for (int e = tid; e < PR_ROWS * CH; e += 128) {
-    const int r = e / CH, c = e % CH;
-    const int gr = row0 + r;
-    cp_async16(smem_u32(sQ) + swz<D>(r, c), gQ + int64_t(min(gr, NK - 1)) * D + c * 8,
-               gr < NK ? 16 : 0);
-  }
-  auto load_k = [&](int t, int stage) {
-    char* dstb = sK + stage * PR_KEYS * D * 2;
-    for (int e = tid; e < PR_KEYS * CH; e += 128) {
-      const int r = e / CH, c = e % CH;
-      const int gr = t * PR_KEYS + r;
-      cp_async16(smem_u32(dstb) + swz<D>(r, c), gK + int64_t(min(gr, NK - 1)) * D + c * 8,
-                 gr < NK ? 16 : 0);
-    }
-  };
-  load_k(0, 0);
-  cp_async_commit();
-  for (int e = tid; e < PR_ROWS * Nb; e += 128) sR[e] = -INFINITY;
-
-  // per-thread rows: g = lane/4 and g+8 of this warp's 16
-  const int g = lane >> 2, qd = lane & 3;
-  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-  uint32_t qa[D / 16][4];
-  const int ntiles = (NK + PR_KEYS - 1) / PR_KEYS;
-
-  for (int t = 0; t < ntiles; ++t) {
-    if (t + 1 < ntiles) load_k(t + 1, (t + 1) & 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (t == 0) {
-#pragma unroll
-      for (int ks_ = 0; ks_ < D / 16; ++ks_) {
-        const int r = warp * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
-        const int c = ks_ * 2 + (lane >> 4);
-        ldsm_x4(smem_u32(sQ) + swz<D>(r, c), qa[ks_][0], qa[ks_][1], qa[ks_][2], qa[ks_][3]);
-      }
-    }
-    const uint32_t kb = smem_u32(sK + (t & 1) * PR_KEYS * D * 2);
-    float s[8][4];
-#pragma unroll
-    for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-#pragma unroll
-    for (int ks_ = 0; ks_ < D / 16; ++ks_) {
-#pragma unroll
-      for (int np = 0; np < 4; ++np) {  // pairs of n8 tiles (16 keys)
-        uint32_t b0, b1, b2, b3;
-        const int r = np * 16 + (lane & 7) + 8 * (lane >> 4);
-        const int c = ks_ * 2 + ((lane >> 3) & 1);
-        ldsm_x4(kb + swz<D>(r, c), b0, b1, b2, b3);
-        mma_bf16(s[2 * np], qa[ks_], b0, b1);
-        mma_bf16(s[2 * np + 1], qa[ks_], b2, b3);
-      }
-    }
-    // scale into the log2 domain, mask invalid sampled keys
-    float tmax[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = t * PR_KEYS + n * 8 + qd * 2 + h;
-        const int jb = col / kk, rr = col - jb * kk;
-        const bool ok = col < NK && rr < min(kk, min(b, N - jb * b));
-        s[n][h] = ok ? s[n][h] * scale_log2 : -INFINITY;
-        s[n][2 + h] = ok ? s[n][2 + h] * scale_log2 : -INFINITY;
-        tmax[0] = fmaxf(tmax[0], s[n][h]);
-        tmax[1] = fmaxf(tmax[1], s[n][2 + h]);
-      }
-    }
-    // R: max over each 16-key group, folded into key block j = col / kk
-#pragma unroll
-    for (int gi = 0; gi < 4; ++gi) {
-#pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        float gm = fmaxf(fmaxf(s[2 * gi][2 * hr], s[2 * gi][2 * hr + 1]),
-                         fmaxf(s[2 * gi + 1][2 * hr], s[2 * gi + 1][2 * hr + 1]));
-        gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 1));
-        gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 2));
-        const int col0 = t * PR_KEYS + gi * 16;
-        if (qd == 0 && col0 < NK) {
-          float* rp = sR + (warp * 16 + g + 8 * hr) * Nb + col0 / kk;
-          *rp = fmaxf(*rp, gm);
-        }
-      }
-    }
-    // online row max / sum (Alg. 3 l.12-15)
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      float tm = tmax[hr];
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 2));
-      const float m_new = fmaxf(m_run[hr], tm);
-      float acc = 0.f;
-      if (m_new != -INFINITY) {
-#pragma unroll
-        for (int n = 0; n < 8; ++n) acc += ex2(s[n][2 * hr] - m_new) + ex2(s[n][2 * hr + 1] - m_new);
-        l_run[hr] = l_run[hr] * ex2(m_run[hr] - m_new) + acc;
-      }
-      m_run[hr] = m_new;
-    }
-    __syncthreads();  // stage (t&1) is refilled by the next iteration's prefetch
-  }
-  // final row stats
-#pragma unroll
-  for (int hr = 0; hr < 2; ++hr) {
-    float l = l_run[hr];
-    l += __shfl_xor_sync(0xffffffffu, l, 1);
-    l += __shfl_xor_sync(0xffffffffu, l, 2);
-    if (qd == 0) {
-      sM[warp * 16 + g + 8 * hr] = m_run[hr];
-      sL[warp * 16 + g + 8 * hr] = l;
-    }
-  }
-  __syncthreads();
-  // max-pool over the k_i valid sampled rows of each query block (Alg. 3 l.17-19)
-  const int rows_here = min(PR_ROWS, NK - row0);
-  const int qb0 = row0 / kk;
-  const int qb1 = (row0 + rows_here - 1) / kk;
-  for (int e = tid; e < (qb1 - qb0 + 1) * Nb; e += 128) {
-    const int ib = qb0 + e / Nb, j = e % Nb;
-    const int ki = min(kk, min(b, N - ib * b));
-    const int r_lo = max(ib * kk, row0), r_hi = min(ib * kk + ki, row0 + rows_here);
-    float best = 0.f;
-    for (int r = r_lo; r < r_hi; ++r) {
-      const int rl = r - row0;
-      best = fmaxf(best, ex2(sR[rl * Nb + j] - sM[rl]) / sL[rl]);
-    }
-    float* dst = pimp + (u * Nb + ib) * int64_t(Nb) + j;
-    if (kk <= PR_ROWS)
-      *dst = best;
-    else
-      atomicMax(reinterpret_cast<int*>(dst), __float_as_int(best));  // positive floats
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K-mask.3  selection (fallback path: after the mma.sync probe; the tcgen05
-// probe selects its own rows in its epilogue).  One warp per row.
+// K-mask.3  selection, one warp per (unit, q-block) row.
 // ---------------------------------------------------------------------------
 constexpr int SEL_WARPS = 4;
 // 6 CTAs per SM (<= 85 registers): the Wan layer's 768 CTAs fit one wave
@@ -878,7 +714,6 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   const int64_t rows = p.BH * p.Nb;
   cudaError_t e;
 
-  const bool p2 = mask_uses_probe2(p);
   {  // K-mask.1 (sampling + gathered copies Q_s, K_s)
     const int64_t warps = p.BH * p.Nb * 2;
     auto kern = p.kk <= 16 ? sample_gather_kernel<D, true> : sample_gather_kernel<D, false>;
@@ -887,33 +722,13 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
         p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
         ks, counters);
   }
-  if (p2) {
-    // K-mask.2: tcgen05 probe (probe2.cu): k in {16, 32, 64}, N_b <= 256
-    e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
-    if (e != cudaSuccess) return e;
-    select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
-        pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags,
-        done, p.neg_flagged);
-  } else {
-    // k = 128 or N_b > 256: the mma.sync probe (R of a 64-row tile in smem)
-    if (p.kk > PR_ROWS) {
-      e = cudaMemsetAsync(pimp, 0, size_t(rows) * p.Nb * 4, stream);
-      if (e != cudaSuccess) return e;
-    }
-    const size_t smem = size_t(PR_ROWS) * D * 2 + 2 * PR_KEYS * D * 2 +
-                        size_t(PR_ROWS) * p.Nb * 4 + 2 * PR_ROWS * 4;
-    e = cudaFuncSetAttribute(probe_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
-    if (e != cudaSuccess) return e;
-    dim3 grid(unsigned((p.Nb * p.kk + PR_ROWS - 1) / PR_ROWS), unsigned(p.BH));
-    probe_kernel<D><<<grid, 128, smem, stream>>>(qs, ks, p.N, p.Nb, p.b, p.kk, p.scale * kLog2e,
-                                                 pimp);
-    // the fallback probe sums l sequentially in fp32 (error up to ~2e-6): never
-    // trust it inside a 2e-5 band
-    select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
-        pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard > 2e-5 ? p.guard : 2e-5, mask, kv_idx,
-        kv_cnt, counters, flags, done, p.neg_flagged);
-  }
+  // K-mask.2: tcgen05 probe (probe2.cu), every supported k and N_b
+  e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
+  if (e != cudaSuccess) return e;
+  // K-mask.3
+  select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
+      pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done,
+      p.neg_flagged);
   if (p.lpt_order) {  // before K-mask.4, so the attention stays its programmatic dependent
     e = launch_lpt_order(kv_cnt, p.BH, p.Nb, D, p.lpt_pairs, p.lpt_order, stream);
     if (e != cudaSuccess) return e;

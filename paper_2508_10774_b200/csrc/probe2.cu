@@ -99,9 +99,12 @@ __global__ void __launch_bounds__(kP2Threads, 1)
     probe2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   int N, int Nb, int b, float scale_log2, float* __restrict__ pimp) {
   using C = P2Cfg<D>;
-  constexpr int G = 128 / KK;              // key blocks per 128-key tile (KK <= 64)
-  constexpr int GH = G / 2;                // key blocks per warp column half
-  static_assert(GH >= 1, "KK <= 64");
+  constexpr int G = KK <= 64 ? 128 / KK : 1;  // key blocks per 128-key tile
+  constexpr int CPB = KK == 128 ? 2 : 1;      // R columns per key block (k = b: one per half)
+  constexpr int CPT = G * CPB;                // R columns per tile
+  constexpr int CPH = CPT / 2;                // R columns per warp column half
+  constexpr int KH = KK <= 64 ? KK : 64;      // keys per R value
+  constexpr int TPP = 256 / CPT;              // tiles per R pass (256 TMEM columns)
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   char* sQ = smem;
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(kP2Threads, 1)
   uint64_t* bar_q = bars;
   uint64_t* bar_full = bars + 1;
   uint64_t* bar_empty = bars + 1 + C::kRing;
-  uint64_t* bar_s = bars + 1 + 2 * C::kRing;  // [2] S buffer (= tile parity) written
+  uint64_t* bar_s = bars + 1 + 2 * C::kRing;  // [2] S buffer (= sequence parity) written
   uint64_t* bar_f = bar_s + 2;                 // [2] S buffer read out (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   float* smm = reinterpret_cast<float*>(smem + C::kOffMisc + 16);  // [4][128]
@@ -123,6 +126,14 @@ __global__ void __launch_bounds__(kP2Threads, 1)
   const int ntiles = (NK + 127) / 128;
   const int k_last = min(KK, N - (Nb - 1) * b);
   const int first_invalid = (Nb - 1) * KK + k_last;  // sampled columns >= this are padding
+  // The tile sequence: pass 0 streams every tile (row statistics, and R of
+  // tiles [0, TPP)); R needs N_b CPB TMEM columns, so when that exceeds 256
+  // (N_b > 256, or k = b with N_b > 128) passes p >= 1 stream tiles
+  // [p TPP, (p+1) TPP) again for their R only (no exponentials), each pass
+  // pooled before the next overwrites the R columns.
+  const int npass = (ntiles + TPP - 1) / TPP;
+  const int nseq = ntiles + (ntiles > TPP ? ntiles - TPP : 0);
+  auto seq_tile = [&](int T) { return T < ntiles ? T : T - ntiles + TPP; };
 
   if (warp == kWarpTma2 && lane == 0) {
     tc::mbar_init(bar_q, 1);
@@ -150,9 +161,9 @@ __global__ void __launch_bounds__(kP2Threads, 1)
       tc::mbar_arrive_expect_tx(bar_q, C::kTile);
       for (int p = 0; p < C::kPanels; ++p)
         tc::tma_load_3d(sQ + p * C::kPanel, &tmQ, bar_q, p * 64, row0, int(u));
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % C::kRing;
-        tc::mbar_wait(bar_empty + s, ((t / C::kRing) & 1) ^ 1);
+      for (int T = 0; T < nseq; ++T) {
+        const int s = T % C::kRing, t = seq_tile(T);
+        tc::mbar_wait(bar_empty + s, ((T / C::kRing) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(bar_full + s, C::kTile);
         for (int p = 0; p < C::kPanels; ++p)
           tc::tma_load_3d(sRing + s * C::kTile + p * C::kPanel, &tmK, bar_full + s, p * 64,
@@ -166,10 +177,10 @@ __global__ void __launch_bounds__(kP2Threads, 1)
       const uint32_t qa = smem_u32(sQ), rb = smem_u32(sRing);
       tc::mbar_wait(bar_q, 0);
       tc::fence_after_sync();
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % C::kRing, bsel = t & 1;
-        tc::mbar_wait(bar_full + s, (t / C::kRing) & 1);
-        if (t >= 2) tc::mbar_wait(bar_f + bsel, ((t >> 1) - 1) & 1);
+      for (int T = 0; T < nseq; ++T) {
+        const int s = T % C::kRing, bsel = T & 1;
+        tc::mbar_wait(bar_full + s, (T / C::kRing) & 1);
+        if (T >= 2) tc::mbar_wait(bar_f + bsel, ((T >> 1) - 1) & 1);
         tc::fence_after_sync();
         const uint32_t kb = rb + s * C::kTile;
 #pragma unroll
@@ -187,140 +198,160 @@ __global__ void __launch_bounds__(kP2Threads, 1)
     const int par = warp >> 3, h = (warp >> 2) & 1, quad = warp & 3;
     const int grp = warp >> 2;  // (par, h): which of the four partial states
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    float m_run = -INFINITY;
-    double l_run = 0.0;
-    const float2 sc2 = make_float2(scale_log2, scale_log2);
-    for (int t = par; t < ntiles; t += 2) {
-      tc::mbar_wait(bar_s + par, (t >> 1) & 1);
-      tc::fence_after_sync();
-      float s[64];
-      {
-        const uint32_t ta = tmem + lane_base + par * 128 + h * 64;
-        uint32_t r0[32], r1[32];
-        tc::ld_32x32b_x32(ta, r0);
-        tc::ld_32x32b_x32(ta + 32, r1);
-        tc::wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          s[e] = __uint_as_float(r0[e]);
-          s[32 + e] = __uint_as_float(r1[e]);
-        }
-      }
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(bar_f + par);  // S buffer may be overwritten now
-      const int col0 = t * 128 + h * 64;
-      if (col0 + 64 > first_invalid) {
-#pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (col0 + c >= first_invalid) s[c] = -INFINITY;
-      }
-      // R: per key-block max of the raw logits (Alg. 3 l.12/l.15)
-      uint32_t rv[GH];
-      float tmax = -INFINITY;
-#pragma unroll
-      for (int g = 0; g < GH; ++g) {
-        float gm = fmax3(s[g * KK], s[g * KK + 1], s[g * KK + 2]);
-#pragma unroll
-        for (int c = 3; c + 1 < KK; c += 2) gm = fmax3(gm, s[g * KK + c], s[g * KK + c + 1]);
-        if ((KK & 1) == 0) gm = fmaxf(gm, s[g * KK + KK - 1]);
-        tmax = fmaxf(tmax, gm);
-        rv[g] = __float_as_uint(gm);
-      }
-      const uint32_t rcol = tmem + lane_base + 256 + t * G + h * GH;
-      if constexpr (GH == 4) {
-        tc::st_32x32b_x4(rcol, reinterpret_cast<uint32_t(&)[4]>(rv));
-      } else if constexpr (GH == 2) {
-        tc::st_32x32b_x2(rcol, reinterpret_cast<uint32_t(&)[2]>(rv));
-      } else {
-        tc::st_32x32b_x1(rcol, reinterpret_cast<uint32_t(&)[1]>(rv));
-      }
-      // online row max / sum over this half tile (l.13-15)
-      const float m_new = fmaxf(m_run, tmax);
-      if (m_new != -INFINITY) {  // a half tile of padding only leaves (M, l) untouched
-        const float2 nm2 = make_float2(-m_new, -m_new);
-#pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float2 x = mul2(add2(make_float2(s[c], s[c + 1]), nm2), sc2);
-          if ((kEmu >> ((c >> 1) & 7)) & 1) {
-            const float2 y = ex2_poly5x2(x);
-            s[c] = y.x;
-            s[c + 1] = y.y;
-          } else {
-            s[c] = ex2(x.x);
-            s[c + 1] = ex2(x.y);
-          }
-        }
-#pragma unroll
-        for (int w = 32; w >= 2; w >>= 1)
-#pragma unroll
-          for (int c = 0; c < w; c += 2) {
-            const float2 y = add2(make_float2(s[c], s[c + 1]), make_float2(s[c + w], s[c + w + 1]));
-            s[c] = y.x;
-            s[c + 1] = y.y;
-          }
-        s[0] += s[1];
-        if (m_new != m_run) l_run *= double(ex2((m_run - m_new) * scale_log2));
-        l_run += double(s[0]);
-        m_run = m_new;
-      }
-    }
-    tc::wait_st();
-    // merge the four partial (M, l) of each row (the l.14 recurrence, once)
     const int r = quad * 32 + lane;
-    smm[grp * 128 + r] = m_run;
-    sml[grp * 128 + r] = l_run;
-    tc::fence_before_sync();  // R columns written by every softmax warp, read below
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kSW * 32) : "memory");
-    tc::fence_after_sync();
-    float M = -INFINITY;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) M = fmaxf(M, smm[g * 128 + r]);
-    double L = 0.0;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const float mg = smm[g * 128 + r];
-      if (mg != -INFINITY) L += sml[g * 128 + r] * double(ex2((mg - M) * scale_log2));
-    }
-    // pooling (l.17-19): v_sj = (R_sj - M_s) c - log2 l_s, P_imp = 2^(max_s v_sj);
-    // rows of query block i are KK consecutive lanes; the four groups take
-    // interleaved 32-column chunks of R
     const int gr = row0 + r;
     const int ib = gr / KK;
     const bool row_ok = gr < NK && (gr % KK) < min(KK, N - ib * b);
-    const float lg = float(log2(L));
-    for (int j0 = grp * 32; j0 < Nb; j0 += 128) {
-      uint32_t rr[32];
-      tc::ld_32x32b_x32(tmem + lane_base + 256 + j0, rr);
-      tc::wait_ld();
-      float pv[32];
+    float m_run = -INFINITY;
+    double l_run = 0.0;
+    float M = 0.f, lg = 0.f;
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
+    for (int pass = 0; pass < npass; ++pass) {
+      const int Ta = pass == 0 ? 0 : ntiles + (pass - 1) * TPP;
+      const int Tb = pass == 0 ? ntiles : ntiles + min(ntiles, (pass + 1) * TPP) - TPP;
+      for (int T = Ta + ((Ta & 1) != par ? 1 : 0); T < Tb; T += 2) {
+        const int t = seq_tile(T);
+        tc::mbar_wait(bar_s + par, (T >> 1) & 1);
+        tc::fence_after_sync();
+        float s[64];
+        {
+          const uint32_t ta = tmem + lane_base + par * 128 + h * 64;
+          uint32_t r0[32], r1[32];
+          tc::ld_32x32b_x32(ta, r0);
+          tc::ld_32x32b_x32(ta + 32, r1);
+          tc::wait_ld();
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        float v = row_ok ? (__uint_as_float(rr[e]) - M) * scale_log2 - lg : -INFINITY;
+          for (int e = 0; e < 32; ++e) {
+            s[e] = __uint_as_float(r0[e]);
+            s[32 + e] = __uint_as_float(r1[e]);
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar_f + par);  // S buffer may be overwritten now
+        const int col0 = t * 128 + h * 64;
+        if (col0 + 64 > first_invalid) {
 #pragma unroll
-        for (int o = 1; o < KK && o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        pv[e] = v;
+          for (int c = 0; c < 64; ++c)
+            if (col0 + c >= first_invalid) s[c] = -INFINITY;
+        }
+        // R: per key-block max of the raw logits (Alg. 3 l.12/l.15); with
+        // k = b one value per half block, the halves combined when pooling
+        uint32_t rv[CPH];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < CPH; ++g) {
+          float gm = fmax3(s[g * KH], s[g * KH + 1], s[g * KH + 2]);
+#pragma unroll
+          for (int c = 3; c + 1 < KH; c += 2) gm = fmax3(gm, s[g * KH + c], s[g * KH + c + 1]);
+          if ((KH & 1) == 0) gm = fmaxf(gm, s[g * KH + KH - 1]);
+          tmax = fmaxf(tmax, gm);
+          rv[g] = __float_as_uint(gm);
+        }
+        if (t >= pass * TPP && t < (pass + 1) * TPP) {  // R of this pass's tiles
+          const uint32_t rcol = tmem + lane_base + 256 + (t - pass * TPP) * CPT + h * CPH;
+          if constexpr (CPH == 4) {
+            tc::st_32x32b_x4(rcol, reinterpret_cast<uint32_t(&)[4]>(rv));
+          } else if constexpr (CPH == 2) {
+            tc::st_32x32b_x2(rcol, reinterpret_cast<uint32_t(&)[2]>(rv));
+          } else {
+            tc::st_32x32b_x1(rcol, reinterpret_cast<uint32_t(&)[1]>(rv));
+          }
+        }
+        if (pass > 0) continue;  // the row statistics are complete after pass 0
+        // online row max / sum over this half tile (l.13-15)
+        const float m_new = fmaxf(m_run, tmax);
+        if (m_new != -INFINITY) {  // a half tile of padding only leaves (M, l) untouched
+          const float2 nm2 = make_float2(-m_new, -m_new);
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const float2 x = mul2(add2(make_float2(s[c], s[c + 1]), nm2), sc2);
+            if ((kEmu >> ((c >> 1) & 7)) & 1) {
+              const float2 y = ex2_poly5x2(x);
+              s[c] = y.x;
+              s[c + 1] = y.y;
+            } else {
+              s[c] = ex2(x.x);
+              s[c + 1] = ex2(x.y);
+            }
+          }
+#pragma unroll
+          for (int w = 32; w >= 2; w >>= 1)
+#pragma unroll
+            for (int c = 0; c < w; c += 2) {
+              const float2 y = add2(make_float2(s[c], s[c + 1]), make_float2(s[c + w], s[c + w + 1]));
+              s[c] = y.x;
+              s[c + 1] = y.y;
+            }
+          s[0] += s[1];
+          if (m_new != m_run) l_run *= double(ex2((m_run - m_new) * scale_log2));
+          l_run += double(s[0]);
+          m_run = m_new;
+        }
       }
-      if (KK > 32) {  // a block spans two warps: max of the two halves (pimp pre-zeroed)
-        if (lane == 0 && ib < Nb) {
+      tc::wait_st();
+      if (pass == 0) smm[grp * 128 + r] = m_run, sml[grp * 128 + r] = l_run;
+      tc::fence_before_sync();  // R columns written by every statistics warp, read below
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kSW * 32) : "memory");
+      tc::fence_after_sync();
+      if (pass == 0) {  // merge the four partial (M, l) of each row (l.14, once)
+        M = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) M = fmaxf(M, smm[g * 128 + r]);
+        double L = 0.0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const float mg = smm[g * 128 + r];
+          if (mg != -INFINITY) L += sml[g * 128 + r] * double(ex2((mg - M) * scale_log2));
+        }
+        lg = float(log2(L));
+      }
+      // pooling (l.17-19): v_sj = (R_sj - M_s) c - log2 l_s, P_imp = 2^(max_s v_sj);
+      // rows of query block i are KK consecutive lanes (k > 32: spread over
+      // warps, combined by atomicMax on the pre-zeroed output); the four
+      // groups take interleaved 32-column chunks of this pass's R
+      const int pc = min(256, Nb * CPB - pass * 256);  // R columns of this pass
+      for (int c0 = grp * 32; c0 < pc; c0 += 128) {
+        uint32_t rr[32];
+        tc::ld_32x32b_x32(tmem + lane_base + 256 + c0, rr);
+        tc::wait_ld();
+        constexpr int NE = 32 / CPB;  // blocks per chunk
+        const int j0 = (pass * 256 + c0) / CPB;
+        float pv[NE];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const float rmax = CPB == 2 ? fmaxf(__uint_as_float(rr[2 * e]), __uint_as_float(rr[2 * e + 1]))
+                                      : __uint_as_float(rr[e]);
+          float v = row_ok ? (rmax - M) * scale_log2 - lg : -INFINITY;
+#pragma unroll
+          for (int o = 1; o < KK && o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+          pv[e] = v;
+        }
+        const int nj = min(NE, Nb - j0);
+        if (KK > 32) {  // a block spans several warps: max over them (pimp pre-zeroed)
+          if (lane == 0 && ib < Nb) {
+            float* dst = pimp + (u * Nb + ib) * int64_t(Nb) + j0;
+            for (int e = 0; e < nj; ++e)
+              atomicMax(reinterpret_cast<int*>(dst + e), __float_as_int(ex2(pv[e])));
+          }
+        } else if ((lane % KK) == 0 && ib < Nb) {
           float* dst = pimp + (u * Nb + ib) * int64_t(Nb) + j0;
-          const int nj = min(32, Nb - j0);
-          for (int e = 0; e < nj; ++e)
-            atomicMax(reinterpret_cast<int*>(dst + e), __float_as_int(ex2(pv[e])));
-        }
-      } else if ((lane % KK) == 0 && ib < Nb) {
-        float* dst = pimp + (u * Nb + ib) * int64_t(Nb) + j0;
-        const int nj = min(32, Nb - j0);
-        if (nj == 32 && (Nb % 4) == 0) {
+          if (nj == 32 && (Nb % 4) == 0) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(dst + e) =
-                make_float4(ex2(pv[e]), ex2(pv[e + 1]), ex2(pv[e + 2]), ex2(pv[e + 3]));
-        } else {
+            for (int e = 0; e < NE; e += 4)
+              *reinterpret_cast<float4*>(dst + e) =
+                  make_float4(ex2(pv[e]), ex2(pv[e + 1]), ex2(pv[e + 2]), ex2(pv[e + 3]));
+          } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e < nj) dst[e] = ex2(pv[e]);
+            for (int e = 0; e < NE; ++e)
+              if (e < nj) dst[e] = ex2(pv[e]);
+          }
         }
+      }
+      if (pass + 1 < npass) {  // R reads of this pass done before the next pass writes R
+        tc::fence_before_sync();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kSW * 32) : "memory");
+        tc::fence_after_sync();
       }
     }
   }
@@ -356,8 +387,8 @@ cudaError_t launch_p2(int64_t BH, int N, int Nb, int b, float scale, const void*
 }  // namespace
 
 bool probe2_supported(int d, int kk, int Nb, int64_t, int) {
-  // R lives in TMEM columns [256, 512): ntiles * (128 / kk) = Nb columns
-  return (d == 64 || d == 128) && (kk == 16 || kk == 32 || kk == 64) && Nb <= 256;
+  // R lives in TMEM columns [256, 512), in passes of 256 columns
+  return (d == 64 || d == 128) && (kk == 16 || kk == 32 || kk == 64 || kk == 128) && Nb <= 512;
 }
 
 cudaError_t launch_probe2(int64_t BH, int N, int Nb, int b, int kk, int d, float scale,
@@ -368,6 +399,8 @@ cudaError_t launch_probe2(int64_t BH, int N, int Nb, int b, int kk, int d, float
   if (d == 64 && kk == 16) return launch_p2<64, 16>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
   if (d == 64 && kk == 32) return launch_p2<64, 32>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
   if (d == 64 && kk == 64) return launch_p2<64, 64>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+  if (d == 128 && kk == 128) return launch_p2<128, 128>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
+  if (d == 64 && kk == 128) return launch_p2<64, 128>(BH, N, Nb, b, scale, qs, ks, pimp, stream);
   return cudaErrorNotSupported;
 }
 

@@ -20,16 +20,21 @@ using namespace blade;
 // mode 7: TS  M128 N64,  B MN-major (the P V form with d = 64)
 // mode 8: as 7, but every group of 8 is committed and waited for (cold start each group)
 // mode 9: SS  M128 N128 groups of 4 (S with d = 64), committed and waited for each group
+// mode 10: the attention skeleton of one block: groups of 8 SS (S, N128) and 8 TS (P V,
+//          N128, B MN-major) alternating, a commit after each group, no waits
+// mode 11: as 10 without the per-group commits
+// mode 12: as 10 with two blocks (S_A, PV_A, S_B, PV_B into separate TMEM columns)
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) issue_loop(int groups, long long* out) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar_g;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < 96 * 1024 / 4; e += 128) reinterpret_cast<uint32_t*>(smem)[e] = 0;
   if (threadIdx.x == 0) {
     tc::mbar_init(&bar, 1);
+    tc::mbar_init(&bar_g, 1);
     tc::fence_barrier_init();
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -38,7 +43,32 @@ __global__ void __launch_bounds__(128, 1) issue_loop(int groups, long long* out)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tslot;
-  if (threadIdx.x == 0) {
+  if (MODE >= 10 && threadIdx.x == 0) {
+    constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0), idO = tc::idesc_bf16(128, 128, 0, 1);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    long long t_start = clock64();
+    for (int g = 0; g < groups; ++g) {
+      const int blk = MODE == 12 ? (g & 1) : 0;
+      const uint32_t dS = tmem + blk * 128, dO = tmem + 256 + blk * 128;
+      if ((g >> (MODE == 12 ? 1 : 0)) & 1) {  // P V group
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          tc::mma_ts(dO, dS + 64 + ks * 8, tc::sw128_desc(b + ks * 2048, 16384, 1024), idO, 1);
+      } else {  // S group
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+          tc::mma_ss(dS, tc::sw128_desc(a + off, 16, 1024), tc::sw128_desc(b + off, 16, 1024),
+                     idS, ks > 0);
+        }
+      }
+      if (MODE != 11) tc::commit(&bar_g);  // arrivals nobody waits for
+    }
+    tc::commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    out[blockIdx.x * 2] = 0;
+    out[blockIdx.x * 2 + 1] = clock64() - t_start;
+  } else if (threadIdx.x == 0) {
     constexpr int N = (MODE == 2 || MODE == 3 || MODE == 7 || MODE == 8) ? 64 : (MODE == 5 ? 256 : 128);
     constexpr bool kMN = MODE == 6 || MODE == 7 || MODE == 8;
     constexpr int G = MODE == 9 ? 4 : 8;
@@ -93,7 +123,7 @@ void run(const char* name) {
   cudaError_t err = cudaDeviceSynchronize();
   long long h[2 * 148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-  const double n = groups * (MODE == 9 ? 4.0 : 8.0);
+  const double n = groups * (MODE == 9 ? 4.0 : 8.0);  // modes 10-12: 8 MMAs per group too
   printf("%-28s issue %.1f cyc/MMA, total %.1f cyc/MMA (%s)\n", name, h[0] / n, h[1] / n,
          cudaGetErrorString(err));
   cudaFree(d);
@@ -111,5 +141,8 @@ int main() {
   run<7>("TS M128 N64 B MN-major");
   run<8>("PV d64 group, cold each");
   run<9>("S d64 group of 4, cold each");
+  run<10>("skeleton 1 block, commits");
+  run<11>("skeleton 1 block, no commits");
+  run<12>("skeleton 2 blocks, commits");
   return 0;
 }
