@@ -125,6 +125,9 @@ blade_status_t blade_bsa_fwd(const void* q, const void* k, const void* v, int64_
   if (!blade::impl_built(impl)) return BLADE_ERR_UNSUPPORTED;
   if (impl == BLADE_ATTN_MMA_SYNC) {
     e = blade::launch_attn_mma(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
+  } else if (impl == BLADE_ATTN_AUTO) {
+    e = blade::launch_attn_auto(p, q, k, v, kv_idx, kv_cnt, o, lse, workspace, s);
+    if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
   } else if (pair) {
     e = blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse, s);
     if (e == cudaErrorNotSupported) return BLADE_ERR_UNSUPPORTED;
@@ -194,6 +197,7 @@ blade_status_t asa_fwd_common(const void* q, const void* k, const void* v, int64
     mp.lpt_order = order;
     mp.lpt_pairs = pair ? 1 : 0;
   }
+  if (impl == BLADE_ATTN_AUTO) mp.attn_work = reinterpret_cast<int*>(ws + mws);
   e = blade::launch_mask(mp, q, k, nullptr, kv_idx, kv_cnt, nullptr, nullptr, nullptr, ws, s);
   if (e != cudaSuccess) return BLADE_ERR_CUDA;
   AttnProblem ap{BH, N, d, mp.b, mp.Nb, mp.scale};
@@ -201,6 +205,9 @@ blade_status_t asa_fwd_common(const void* q, const void* k, const void* v, int64
     e = blade::launch_attn_mma(ap, q, k, v, kv_idx, kv_cnt, o, lse, s);
   } else if (impl == BLADE_ATTN_TCGEN05_TRIPLE) {
     e = blade::launch_attn_tc3(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, gt);
+  } else if (impl == BLADE_ATTN_AUTO) {
+    e = blade::launch_attn_auto(ap, q, k, v, kv_idx, kv_cnt, o, lse, ws + mws, s, gt, true,
+                                order, /*work_zeroed=*/true);
   } else if (pair) {
     e = blade::launch_attn_tc2(ap, q, k, v, kv_idx, kv_cnt, o, lse, s, gt, true, order);
   } else {
@@ -274,7 +281,10 @@ blade_status_t blade_bsa_gt_fwd(const void* q, const void* k, const void* v, int
       impl == BLADE_ATTN_TCGEN05_TRIPLE
           ? blade::launch_attn_tc3(p, q, k, v, kv_idx, kv_cnt, o, lse,
                                    static_cast<cudaStream_t>(stream), &g)
-      : (impl == BLADE_ATTN_TCGEN05_PAIR || impl == BLADE_ATTN_AUTO)
+      : impl == BLADE_ATTN_AUTO
+          ? blade::launch_attn_auto(p, q, k, v, kv_idx, kv_cnt, o, lse, workspace,
+                                    static_cast<cudaStream_t>(stream), &g)
+      : impl == BLADE_ATTN_TCGEN05_PAIR
           ? blade::launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse,
                                    static_cast<cudaStream_t>(stream), &g)
           : blade::launch_attn_tc(p, q, k, v, kv_idx, kv_cnt, o, lse,

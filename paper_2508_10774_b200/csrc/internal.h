@@ -22,6 +22,7 @@ struct MaskProblem {
   int neg_flagged;  // blade_asa_fwd: refined rows' kv_cnt provisional (-1 - m) until K-mask.4
   int32_t* lpt_order;  // blade_asa_fwd: LPT order of the attention CTAs, written before K-mask.4
   int lpt_pairs;       // order over pairs of query blocks (two-block kernel)
+  int* attn_work;      // blade_asa_fwd: the persistent attention's item counter, zeroed by K-mask.1
 };
 
 // Workspace carve-up for blade_asa_mask (all offsets 256-byte aligned).
@@ -106,6 +107,32 @@ cudaError_t launch_attn_tc2(const AttnProblem& p, const void* q, const void* k, 
                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
                             cudaStream_t stream, const GtProblem* gt = nullptr, bool pdl = false,
                             const int32_t* order = nullptr);
+
+// The pair kernel as a persistent kernel (attn_tc2p.cu): one CTA per SM
+// claims (unit, pair) items from the counter `work` (an int of the attention
+// workspace, zeroed on the stream by the launcher); BLADE_ATTN_AUTO uses it.
+cudaError_t launch_attn_tc2p(const AttnProblem& p, const void* q, const void* k, const void* v,
+                             const int32_t* kv_idx, const int32_t* kv_cnt, void* o, float* lse,
+                             int* work, bool work_zeroed, cudaStream_t stream,
+                             const GtProblem* gt = nullptr, bool pdl = false,
+                             const int32_t* order = nullptr);
+// work_zeroed: K-mask.1 of the same call zeroed the counter (blade_asa_fwd; a
+// memset here would sit between K-mask.4 and the attention and break the
+// programmatic dependent launch), else it is zeroed here.
+inline cudaError_t launch_attn_auto(const AttnProblem& p, const void* q, const void* k,
+                                    const void* v, const int32_t* kv_idx, const int32_t* kv_cnt,
+                                    void* o, float* lse, void* workspace, cudaStream_t stream,
+                                    const GtProblem* gt = nullptr, bool pdl = false,
+                                    const int32_t* order = nullptr, bool work_zeroed = false) {
+#ifdef BLADE_ATTN2P_OFF  // A/B: the non-persistent pair kernel
+  (void)workspace;
+  (void)work_zeroed;
+  return launch_attn_tc2(p, q, k, v, kv_idx, kv_cnt, o, lse, stream, gt, pdl, order);
+#else
+  return launch_attn_tc2p(p, q, k, v, kv_idx, kv_cnt, o, lse, static_cast<int*>(workspace),
+                          work_zeroed, stream, gt, pdl, order);
+#endif
+}
 
 // Longest-processing-time order of the attention CTAs (one query block, or a
 // pair of blocks when pairs != 0) by kept-block count, descending; counts may

@@ -97,14 +97,17 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, int64_t BH,
     int N, int Nb, int b, int kk, uint64_t seed, int mode, int share_qk, int64_t unit_offset,
     int32_t* __restrict__ sample_idx, __nv_bfloat16* __restrict__ qs,
-    __nv_bfloat16* __restrict__ ks, int* __restrict__ counters) {
+    __nv_bfloat16* __restrict__ ks, int* __restrict__ counters, int* __restrict__ attn_work) {
   __shared__ int offs[8][128];
   __shared__ uint32_t sel_bits[8][4];
   __shared__ uint64_t cand_h[8][64];
   __shared__ int cand_o[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * 8 + warp;
-  if (w == 0 && lane == 0) counters[0] = 0;  // refine queue length
+  if (w == 0 && lane == 0) {
+    counters[0] = 0;                     // refine queue length
+    if (attn_work) attn_work[0] = 0;     // the persistent attention's item counter
+  }
   const bool active = w < BH * Nb * 2;
   const int which = int(w & 1);
   const int64_t rest = w >> 1;
@@ -720,7 +723,7 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
     kern<<<unsigned((warps + 7) / 8), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
         p.BH, p.N, p.Nb, p.b, p.kk, p.seed, p.mode, p.share_qk, p.unit_offset, sample_idx, qs,
-        ks, counters);
+        ks, counters, p.attn_work);
   }
   // K-mask.2: tcgen05 probe (probe2.cu), every supported k and N_b
   e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);

@@ -97,3 +97,32 @@ def test_fused_many_ctas_mixed_refined_rows(A, d, impl):
         assert torch.equal(cnt, m.kv_cnt) and torch.equal(idx, m.kv_idx)
         assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
         assert torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("keep", [None, 3])
+def test_fused_persistent_many_items_per_cta(A, d, keep):
+    """The AUTO attention is persistent (one CTA per SM walking the (unit,
+    pair) items): 96 units x 4 pairs = 384 items, 2-3 per CTA, so TMEM, the
+    K/V rings and every barrier phase carry across items, refined rows (whose
+    CTA waits for K-mask.4) sit between unrefined ones, tau mode activates the
+    LPT order (alternating rounds); the result must equal the separate calls
+    and the non-persistent pair kernel (impl PAIR) bit for bit."""
+    q, k, v = inputs.smooth(1, 96, 1000, d, (1, 1, 1000), ell=3.0, beta=9.0, seed=5 + d)
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    kw = dict(tau=0.9, keep_min=1, refine_guard=1e-3) if keep is None else \
+        dict(tau=0.9, keep_min=keep, keep_max=keep, refine_guard=1e-3)
+    o1, l1, m = A.asa_forward(qd, kd, vd, **kw)
+    n_ref = int(m.n_refined.item())
+    assert 0 < n_ref < 96 * 8, n_ref
+    o3 = torch.empty_like(qd)
+    l3 = torch.empty_like(l1)
+    A.blade_bsa_fwd(qd, kd, vd, m.kv_idx, m.kv_cnt, impl=A.ATTN_TCGEN05_PAIR, o=o3, lse=l3)
+    for _ in range(2):
+        o2, l2, idx, cnt = A.blade_asa_fwd(qd, kd, vd, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(cnt, m.kv_cnt) and torch.equal(idx, m.kv_idx)
+        assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+        assert torch.equal(l1, l2)
+    assert torch.equal(o1.view(torch.int16), o3.view(torch.int16))
+    assert torch.equal(l1, l3)
