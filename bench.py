@@ -527,7 +527,8 @@ def measure_layer(args, workload: str, dev, local: int, *, headline: bool):
                "ms_per_step": e2e_ms, "api": "blade_asa_fwd_host (C ABI, pinned host buffers, "
                "chunked copy/compute overlap)", "h2d_bytes_per_step": 3 * q_h.numel() * 2,
                "d2h_bytes_per_step": q_h.numel() * 2 + BH * N * 4}
-    roof = {"kernel": "attn_tc2_kernel (blade_bsa_fwd)", "bound": "tensor",
+    roof = {"kernel": "attn_tc2p_kernel (persistent pair kernel, blade_bsa_fwd AUTO)",
+            "bound": "tensor",
             "achieved": attn_tflops, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
             "frac": attn_tflops / pk["bf16_tflops"],
             "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)",

@@ -23,7 +23,9 @@
  *     units is a contiguous slice.  Q, K, V, O are bf16 (raw 16-bit words).
  *   - Nothing is allocated or freed by the library.  Scratch comes from the
  *     caller's `workspace` (device memory, >= the size the matching
- *     *_workspace_size() returns, 256-byte aligned).
+ *     *_workspace_size() returns, 256-byte aligned).  The library writes it
+ *     (e.g. the persistent attention's item counter), so one workspace must
+ *     not serve two calls that can run concurrently (different streams).
  *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
  *     stream).  Calls never synchronise the host.
  *   - Arguments are validated synchronously before anything is enqueued; a
@@ -108,7 +110,9 @@ blade_status_t blade_asa_mask(const void* q, const void* k, int64_t BH, int32_t 
 size_t blade_bsa_fwd_workspace_size(int64_t BH, int32_t N, int32_t d, int32_t block);
 
 /* Attention implementations (the `impl` argument of blade_bsa_fwd). */
-#define BLADE_ATTN_AUTO 0      /* fastest measured: TCGEN05_PAIR for d = 64 and 128     */
+#define BLADE_ATTN_AUTO 0      /* fastest measured, d = 64 and 128: the pair schedule of
+                                  TCGEN05_PAIR as a persistent kernel (one CTA per SM
+                                  claiming (unit, pair of query blocks) items)          */
 #define BLADE_ATTN_TCGEN05 1   /* sm_100a tcgen05 + TMEM + TMA warp-specialised kernel */
 #define BLADE_ATTN_MMA_SYNC 2  /* legacy mma.sync baseline (BLADE_WITH_BASELINES builds)  */
 #define BLADE_ATTN_TCGEN05_PAIR 3 /* tcgen05 kernel with two query blocks per CTA (ping-pong) */

@@ -55,6 +55,9 @@ struct CfgP {
   static constexpr uint32_t kColO = 256;
 };
 constexpr int kThreadsP = 384;
+#ifndef BLADE_ATTN2P_QPREFETCH
+#define BLADE_ATTN2P_QPREFETCH 1  // L2 prefetch of the next item's Q while its slot drains
+#endif
 constexpr float kRescaleThresholdP = 8.0f;  // log2 units
 // exponential pairs on the FMA pipe (as attn_tc2.cu): 1 in 8 for d = 64
 constexpr uint32_t kEmuMaskP64 = 0x01, kEmuMaskP128 = 0x00;
@@ -213,7 +216,12 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           }
           if (!get_item(x, it)) break;
           if (isK) {  // Q_A, Q_B of this item, once the previous item's S MMAs are done
-            if (n > 0) tc::mbar_wait(bar_qfree, (n - 1) & 1);
+            if (n > 0) {  // meanwhile pull them into L2
+              for (int t = 0; t < (BLADE_ATTN2P_QPREFETCH ? it.nblk : 0); ++t)
+                for (int p = 0; p < C::kPanels; ++p)
+                  tc::tma_prefetch_3d(&tmQ, p * 64, (it.i0 + t) * 128, int(it.u));
+              tc::mbar_wait(bar_qfree, (n - 1) & 1);
+            }
             tc::mbar_arrive_expect_tx(bar_q, it.nblk * C::kTile);
             for (int t = 0; t < it.nblk; ++t)
               for (int p = 0; p < C::kPanels; ++p)
