@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(256) sample_gather_kernel(
   __shared__ int cand_o[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * 8 + warp;
+  // K-mask.2 (probe2_kernel, a programmatic dependent) may be scheduled now;
+  // its producer waits for this grid's completion before reading Q_s / K_s
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (w == 0 && lane == 0) {
     counters[0] = 0;                     // refine queue length
     if (attn_work) attn_work[0] = 0;     // the persistent attention's item counter
@@ -245,6 +248,9 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, BLADE_SEL_MIN_BLOCKS) select_k
   __shared__ uint32_t keep_bits[SEL_WARPS][16];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * SEL_WARPS + warp;
+  // a programmatic dependent of K-mask.2: P_imp (and the zeroed refine queue
+  // counter of K-mask.1, complete before K-mask.2 began) visible past this
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (row >= rows) return;
   const bool flag = select_row(pimp + row * Nb, Nb, tau, lo, hi, guard, true,
                                mask ? mask + row * Nb : nullptr, kv_idx + row * Nb, kv_cnt + row,
@@ -729,9 +735,21 @@ cudaError_t launch_mask_d(const MaskProblem& p, const void* q, const void* k, ui
   e = launch_probe2(p.BH, p.N, p.Nb, p.b, p.kk, D, p.scale, qs, ks, pimp, stream);
   if (e != cudaSuccess) return e;
   // K-mask.3
-  select_kernel<<<unsigned((rows + SEL_WARPS - 1) / SEL_WARPS), SEL_WARPS * 32, 0, stream>>>(
-      pimp, rows, p.Nb, p.tau, p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done,
-      p.neg_flagged);
+  {  // K-mask.3, a programmatic dependent of K-mask.2 (its launch overlaps the probe's tail)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((rows + SEL_WARPS - 1) / SEL_WARPS));
+    cfg.blockDim = dim3(SEL_WARPS * 32);
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, select_kernel, static_cast<const float*>(pimp), rows, p.Nb, p.tau,
+                           p.lo, p.hi, p.guard, mask, kv_idx, kv_cnt, counters, flags, done,
+                           p.neg_flagged);
+    if (e != cudaSuccess) return e;
+  }
   if (p.lpt_order) {  // before K-mask.4, so the attention stays its programmatic dependent
     e = launch_lpt_order(kv_cnt, p.BH, p.Nb, D, p.lpt_pairs, p.lpt_order, stream);
     if (e != cudaSuccess) return e;

@@ -152,12 +152,17 @@ __global__ void __launch_bounds__(kP2Threads, 1)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  // K-mask.3 (select_kernel, a programmatic dependent) may be scheduled now;
+  // it waits for this grid's completion before reading P_imp
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   if (warp == kWarpTma2) {
     // ===================== producer: tiled TMA loads of Q_s / K_s =====
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmQ);
       tc::tma_prefetch_desc(&tmK);
+      // a programmatic dependent of K-mask.1: Q_s / K_s complete past this
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
       tc::mbar_arrive_expect_tx(bar_q, C::kTile);
       for (int p = 0; p < C::kPanels; ++p)
         tc::tma_load_3d(sQ + p * C::kPanel, &tmQ, bar_q, p * 64, row0, int(u));
@@ -379,8 +384,21 @@ cudaError_t launch_p2(int64_t BH, int N, int Nb, int b, float scale, const void*
     if (e != cudaSuccess) return e;
   }
   dim3 grid(unsigned((NK + 127) / 128), unsigned(BH));
-  probe2_kernel<D, KK><<<grid, kP2Threads, smem, stream>>>(mq, mk, N, Nb, b,
-                                                           scale * 1.4426950408889634f, pimp);
+  // programmatic dependent launch behind K-mask.1 (sample_gather_kernel): the
+  // prologue (barriers, TMEM, descriptor prefetch) overlaps its tail
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kP2Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, probe2_kernel<D, KK>, mq, mk, N, Nb, b,
+                         scale * 1.4426950408889634f, pimp);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
