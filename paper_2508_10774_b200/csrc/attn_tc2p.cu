@@ -60,7 +60,13 @@ constexpr int kThreadsP = 384;
 #endif
 constexpr float kRescaleThresholdP = 8.0f;  // log2 units
 // exponential pairs on the FMA pipe (as attn_tc2.cu): 1 in 8 for d = 64
-constexpr uint32_t kEmuMaskP64 = 0x01, kEmuMaskP128 = 0x00;
+#ifndef BLADE_ATTN2P_EMU64
+#define BLADE_ATTN2P_EMU64 0x01
+#endif
+#ifndef BLADE_ATTN2P_EMU128
+#define BLADE_ATTN2P_EMU128 0x00
+#endif
+constexpr uint32_t kEmuMaskP64 = BLADE_ATTN2P_EMU64, kEmuMaskP128 = BLADE_ATTN2P_EMU128;
 
 // One item = query blocks A = 2x, B = 2x + 1 of one unit.
 struct PairItem {
