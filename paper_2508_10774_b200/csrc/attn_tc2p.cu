@@ -36,6 +36,12 @@ using attn::DefaultScale;
 using attn::ex2_poly2;
 using attn::GtArgs;
 
+#ifndef BLADE_ATTN2P_SEPP
+#define BLADE_ATTN2P_SEPP 1  // d = 64: P outside S (below); Cog attention 0.920-0.926 vs 0.948 ms
+#endif
+
+constexpr int kThreadsP = 384;  // 8 softmax warps, MMA issuer, K / Q and V producers, spare
+
 template <int D>
 struct CfgP {
   static constexpr int kTile = 128 * D * 2;  // one Q / K / V tile
@@ -47,14 +53,23 @@ struct CfgP {
   static constexpr int kOffRingK = 2 * kTile;
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
   static constexpr int kOffBar = kOffRingV + kRingV * kTile;
-  // bar_q, bar_qfree, kfull/kempty, vfull/vempty, per block: s, p, pv, item queue full/empty
-  static constexpr int kNumBar = 2 + 2 * kRingK + 2 * kRingV + 3 * 2 + 2 * 4;
+  // bar_q, bar_qfree, kfull/kempty, vfull/vempty, per block: s, p, pv, sf, item queue full/empty
+  static constexpr int kNumBar = 2 + 2 * kRingK + 2 * kRingV + 4 * 2 + 2 * 4;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;   // tmem slot (16 B)
   static constexpr int kOffItems = kOffMisc + 16;           // int [4] claimed item queue
   static constexpr int kSmem = kOffItems + 16 + 1024;       // + alignment slack
   static constexpr uint32_t kColO = 256;
+  // registers: the kernel runs at 168, the four role warps drop to
+  // kRegLow, the softmax warps take the rest
+  static constexpr int kRegLow = 72;
+  static constexpr int kRegHigh = 216;
+  // d = 64 leaves TMEM room for P outside S: P_t at [256 + 2d + 64t, +64).
+  // S_t(n+1) is then issued as soon as the softmax has read S_t(n) (bar_sf),
+  // and the softmax waits for P V_t(n-1) only right before it stores P_t(n),
+  // so a block's softmax runs tile after tile without the S round trip.
+  static constexpr bool kSepP = D == 64 && BLADE_ATTN2P_SEPP;
+  static constexpr uint32_t kColP = 256 + 2 * D;
 };
-constexpr int kThreadsP = 384;
 #ifndef BLADE_ATTN2P_QPREFETCH
 #define BLADE_ATTN2P_QPREFETCH 1  // L2 prefetch of the next item's Q while its slot drains
 #endif
@@ -103,7 +118,8 @@ __global__ void __launch_bounds__(kThreadsP, 1)
   uint64_t* bar_s = bar_vempty + C::kRingV;  // [2] S of block t computed
   uint64_t* bar_p = bar_s + 2;               // [2] P of block t written (4 warp arrivals)
   uint64_t* bar_pv = bar_p + 2;              // [2] last P V of block t in an item done
-  uint64_t* bar_ifull = bar_pv + 2;          // [4] item queue slot written (warp 9)
+  uint64_t* bar_sf = bar_pv + 2;             // [2] S_t read out by its 4 softmax warps (kSepP)
+  uint64_t* bar_ifull = bar_sf + 2;          // [4] item queue slot written (warp 9)
   uint64_t* bar_iempty = bar_ifull + 4;      // [4] slot read by the other 10 warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   int* sItem = reinterpret_cast<int*>(smem + C::kOffItems);
@@ -171,6 +187,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
       tc::mbar_init(bar_s + t, 1);
       tc::mbar_init(bar_p + t, 4);
       tc::mbar_init(bar_pv + t, 1);
+      tc::mbar_init(bar_sf + t, 4);
     }
     for (int i = 0; i < 4; ++i) {
       tc::mbar_init(bar_ifull + i, 1);
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
     // the CTA holds 384 x 168 registers: 128 x (168 - 72) freed here cover the
     // 256 x (216 - 168) the softmax warpgroups take (setmaxnreg.inc blocks
     // until the pool has them)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::kRegLow) : "memory");
     if (warp == 9 || warp == 10) {
       // ===================== TMA producers (warp 9: Q and K, warp 10: V) =====
       if (lane == 0) {
@@ -266,6 +283,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
         const uint32_t qbase = smem_u32(sQ), kbase = smem_u32(sRingK), vbase = smem_u32(sRingV);
         int gk = 0, gv = 0;         // ring positions, continuous over the items
         int np[2] = {0, 0};         // bar_p phases consumed per block
+        int gs[2] = {0, 0};         // S_t issued so far (kSepP: bar_sf phases)
         PairItem it;
         for (int n = 0; get_item(take_item(n, BLADE_MMA_WARP != 0), it); ++n) {
           tc::mbar_wait(bar_q, n & 1);
@@ -273,6 +291,8 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           int s_left = it.cnt0 + it.cnt1;  // S MMAs of this item still to issue
           auto issue_S = [&](int t) {  // S_t = Q_t K^T of block t's next tile
             const int s = gk % C::kRingK;
+            if (C::kSepP && gs[t] > 0) tc::mbar_wait(bar_sf + t, (gs[t] - 1) & 1);  // S_t read
+            ++gs[t];
             tc::mbar_wait(bar_kfull + s, (gk / C::kRingK) & 1);
             tc::fence_after_sync();
             const uint32_t kb = kbase + s * C::kTile, qb = qbase + t * C::kTile;
@@ -296,12 +316,14 @@ __global__ void __launch_bounds__(kThreadsP, 1)
             const uint32_t vb = vbase + s * C::kTile;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              BLADE_MMA_TS(tmem + C::kColO + t * D, tmem + t * 128 + 64 + ks * 8,
+              BLADE_MMA_TS(tmem + C::kColO + t * D,
+                           tmem + (C::kSepP ? C::kColP + t * 64 : t * 128 + 64) + ks * 8,
                            tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                            (k > 0 || ks > 0) ? 1 : 0);
-            // only the item's last P V is awaited (the epilogue): S(k+1) is
-            // issued after P V(k) and one thread's tcgen05 ops complete in order
-            if (k + 1 == (t ? it.cnt1 : it.cnt0)) BLADE_COMMIT(bar_pv + t);
+            // without kSepP only the item's last P V is awaited (the epilogue):
+            // S(k+1) is issued after P V(k) and one thread's tcgen05 ops
+            // complete in order; with kSepP the softmax waits for every P V
+            if (C::kSepP || k + 1 == (t ? it.cnt1 : it.cnt0)) BLADE_COMMIT(bar_pv + t);
             BLADE_COMMIT(bar_vempty + s);
             ++gv;
           };
@@ -310,6 +332,15 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           if (it.cnt1 > 0) issue_S(1);
           const int m = it.cnt0 > it.cnt1 ? it.cnt0 : it.cnt1;
           for (int k = 0; k < m; ++k) {
+            if (C::kSepP) {
+              // S(k+1) of both blocks as soon as S(k) has been read out, then
+              // the P V of tile k
+              if (k + 1 < it.cnt0) issue_S(0);
+              if (k + 1 < it.cnt1) issue_S(1);
+              if (k < it.cnt0) issue_PV(0, k);
+              if (k < it.cnt1) issue_PV(1, k);
+              continue;
+            }
             if (k < it.cnt0) {
               issue_PV(0, k);
               if (k + 1 < it.cnt0) issue_S(0);
@@ -323,12 +354,15 @@ __global__ void __launch_bounds__(kThreadsP, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::kRegHigh) : "memory");
     // ===================== softmax of block t =====================
+    // warp (t, qw): rows 32 qw .. 32 qw + 31 (TMEM lane quarter qw) of block t
     const int t = warp >> 2, qw = warp & 3;
     const uint32_t lane_base = uint32_t(qw * 32) << 16;
     const uint32_t tS = tmem + lane_base + t * 128;
     const uint32_t tO = tmem + lane_base + C::kColO + t * D;
+    // P over the upper half of S_t, or (kSepP) in its own columns
+    const uint32_t tP = C::kSepP ? tmem + lane_base + C::kColP + t * 64 : tS + 64;
     const int r = qw * 32 + lane;
     const float2 sl2 = make_float2(scale_log2, scale_log2);
     int ns = 0, npv = 0;  // bar_s / bar_pv phases consumed
@@ -354,6 +388,12 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
         }
         tc::wait_ld();
+        if (C::kSepP) {  // S_t's columns may be overwritten by S_t(n+1) now
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(bar_sf + t);
+        }
+        bool pv_done = !C::kSepP || n == 0;  // P V_t(n-1) complete (kSepP)
         const bool fine = !kGT || n < cnt_fine;
         const int valid = fine ? N - jb * 128 : gt.Ng - (n - cnt_fine) * 128;
         if (valid < 128) {
@@ -381,10 +421,17 @@ __global__ void __launch_bounds__(kThreadsP, 1)
         }
         const float mxs = mx * scale_log2;
         // warp-uniform (tcgen05.ld/st are .sync.aligned); always true for n = 0.
-        // O_t is current: S_t(n) was issued after P V_t(n-1) and has completed.
+        // O_t is current: S_t(n) was issued after P V_t(n-1) and has completed
+        // (kSepP: waited for here).
         if (__any_sync(0xffffffffu, mxs > m_used + kRescaleThresholdP)) {
           const float m_new = fmaxf(m_used, mxs);
           if (n > 0) {
+            if (!pv_done) {
+              tc::mbar_wait(bar_pv + t, npv & 1);
+              ++npv;
+              tc::fence_after_sync();
+              pv_done = true;
+            }
             const float f = ex2(m_used - m_new);
             l_sum *= f;
 #pragma unroll
@@ -418,7 +465,12 @@ __global__ void __launch_bounds__(kThreadsP, 1)
             acc4[e & 3] = add2(acc4[e & 3], pp);
             pk[e] = pack_bf16(pp.x, pp.y);
           }
-          tc::st_32x32b_x16(tS + 64 + c * 16, pk);
+          if (c == 0 && !pv_done) {  // kSepP: P_t's columns are free once P V_t(n-1) is done
+            tc::mbar_wait(bar_pv + t, npv & 1);
+            ++npv;
+            tc::fence_after_sync();
+          }
+          tc::st_32x32b_x16(tP + c * 16, pk);
         }
         const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
         l_sum += acc.x + acc.y;
