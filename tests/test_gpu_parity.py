@@ -24,7 +24,8 @@ def A(cuda_dev):
 
 # the product kernels (AUTO = the pair kernel); the mma.sync and three-S-buffer
 # baselines are compiled only into -DBLADE_WITH_BASELINES builds
-IMPLS = [pytest.param(1, id="tcgen05"), pytest.param(3, id="pair")]
+# AUTO = the persistent pair kernel (attn_tc2p.cu), the product default
+IMPLS = [pytest.param(1, id="tcgen05"), pytest.param(3, id="pair"), pytest.param(0, id="auto")]
 
 
 def _run_mask(A, q, k, p: O.AsaParams, **kw):
