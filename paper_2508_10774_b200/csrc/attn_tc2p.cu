@@ -36,6 +36,9 @@ using attn::DefaultScale;
 using attn::ex2_poly2;
 using attn::GtArgs;
 
+#ifndef BLADE_ATTN2P_PCHUNK
+#define BLADE_ATTN2P_PCHUNK 1  // d = 128: P handed over in 1, 2 or 4 key chunks
+#endif
 #ifndef BLADE_ATTN2P_SEPP
 #define BLADE_ATTN2P_SEPP 1  // d = 64: P outside S (below); Cog attention 0.920-0.926 vs 0.948 ms
 #endif
@@ -54,7 +57,7 @@ struct CfgP {
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
   static constexpr int kOffBar = kOffRingV + kRingV * kTile;
   // bar_q, bar_qfree, kfull/kempty, vfull/vempty, per block: s, p, pv, sf, item queue full/empty
-  static constexpr int kNumBar = 2 + 2 * kRingK + 2 * kRingV + 4 * 2 + 2 * 4;
+  static constexpr int kNumBar = 2 + 2 * kRingK + 2 * kRingV + 4 * 2 + 3 * 2 + 2 * 4;
   static constexpr int kOffMisc = kOffBar + kNumBar * 8;   // tmem slot (16 B)
   static constexpr int kOffItems = kOffMisc + 16;           // int [4] claimed item queue
   static constexpr int kSmem = kOffItems + 16 + 1024;       // + alignment slack
@@ -69,6 +72,8 @@ struct CfgP {
   // so a block's softmax runs tile after tile without the S round trip.
   static constexpr bool kSepP = D == 64 && BLADE_ATTN2P_SEPP;
   static constexpr uint32_t kColP = 256 + 2 * D;
+  // P V of block t's tile issued chunk by chunk as the softmax stores P
+  static constexpr int kPChunks = kSepP ? 1 : BLADE_ATTN2P_PCHUNK;
 };
 #ifndef BLADE_ATTN2P_QPREFETCH
 #define BLADE_ATTN2P_QPREFETCH 1  // L2 prefetch of the next item's Q while its slot drains
@@ -119,7 +124,8 @@ __global__ void __launch_bounds__(kThreadsP, 1)
   uint64_t* bar_p = bar_s + 2;               // [2] P of block t written (4 warp arrivals)
   uint64_t* bar_pv = bar_p + 2;              // [2] last P V of block t in an item done
   uint64_t* bar_sf = bar_pv + 2;             // [2] S_t read out by its 4 softmax warps (kSepP)
-  uint64_t* bar_ifull = bar_sf + 2;          // [4] item queue slot written (warp 9)
+  uint64_t* bar_ph = bar_sf + 2;             // [2][3] P_t chunk c < kPChunks - 1 written (4 warps)
+  uint64_t* bar_ifull = bar_ph + 6;          // [4] item queue slot written (warp 9)
   uint64_t* bar_iempty = bar_ifull + 4;      // [4] slot read by the other 10 warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   int* sItem = reinterpret_cast<int*>(smem + C::kOffItems);
@@ -188,6 +194,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
       tc::mbar_init(bar_p + t, 4);
       tc::mbar_init(bar_pv + t, 1);
       tc::mbar_init(bar_sf + t, 4);
+      for (int c = 0; c < 3; ++c) tc::mbar_init(bar_ph + 3 * t + c, 4);
     }
     for (int i = 0; i < 4; ++i) {
       tc::mbar_init(bar_ifull + i, 1);
@@ -310,16 +317,21 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           auto issue_PV = [&](int t, int k) {  // O_t += P_t V of block t's tile k
             const int s = gv % C::kRingV;
             tc::mbar_wait(bar_vfull + s, (gv / C::kRingV) & 1);
-            tc::mbar_wait(bar_p + t, np[t] & 1);
-            ++np[t];
-            tc::fence_after_sync();
             const uint32_t vb = vbase + s * C::kTile;
+            constexpr int kPer = 8 / C::kPChunks;  // MMAs (16 keys each) per chunk
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
+            for (int ks = 0; ks < 8; ++ks) {
+              if (ks % kPer == 0) {  // this chunk of P stored
+                const int c = ks / kPer;
+                tc::mbar_wait(c == C::kPChunks - 1 ? bar_p + t : bar_ph + 3 * t + c, np[t] & 1);
+                tc::fence_after_sync();
+              }
               BLADE_MMA_TS(tmem + C::kColO + t * D,
                            tmem + (C::kSepP ? C::kColP + t * 64 : t * 128 + 64) + ks * 8,
                            tc::sw128_desc(vb + ks * 2048, C::kPanel, 1024), idO,
                            (k > 0 || ks > 0) ? 1 : 0);
+            }
+            ++np[t];
             // without kSepP only the item's last P V is awaited (the epilogue):
             // S(k+1) is issued after P V(k) and one thread's tcgen05 ops
             // complete in order; with kSepP the softmax waits for every P V
@@ -471,6 +483,13 @@ __global__ void __launch_bounds__(kThreadsP, 1)
             tc::fence_after_sync();
           }
           tc::st_32x32b_x16(tP + c * 16, pk);
+          constexpr int kCPer = 4 / C::kPChunks;  // 32-key store chunks per P chunk
+          if (C::kPChunks > 1 && c % kCPer == kCPer - 1 && c < 3) {  // P V of this chunk may start
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(bar_ph + 3 * t + c / kCPer);
+          }
         }
         const float2 acc = add2(add2(acc4[0], acc4[1]), add2(acc4[2], acc4[3]));
         l_sum += acc.x + acc.y;
