@@ -1,7 +1,8 @@
-# Round-2 final evidence refresh (product build): GPU suite, smoke, bench lines, mask and
-# backward timings, launch lists, pipe counters, ncu full captures.
-mkdir -p gpurun_out/r02f3
-P=gpurun_out/r02f3
+# End-of-round evidence on one B200 (product build): GPU suite, smoke, bench lines, mask and
+# backward timings, sparsity sweep, launch lists, pipe counters, ncu full captures.
+#   gpurun --timeout 3000 -- 'bash scripts/gpu_round_evidence.sh [outdir]'
+P=${1:-gpurun_out/evidence}
+mkdir -p $P
 python -c "import __graft_entry__ as g; g.build()" > $P/build.log 2>&1
 timeout 1800 python -m pytest tests -m gpu -q > $P/pytest_gpu.log 2>&1; echo "rc=$?" >> $P/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $P/smoke.log 2>&1
@@ -14,6 +15,10 @@ python scripts/mask_time.py --workload wan > $P/mask_time_wan.jsonl 2>&1
 python scripts/mask_time.py --workload cog --configs keep25,tau0.9,tau0.95 > $P/mask_time_cog.jsonl 2>&1
 python scripts/bench_bwd.py > $P/bench_bwd_wan.json 2>&1
 python scripts/bench_bwd.py --workload cog > $P/bench_bwd_cog.json 2>&1
+python scripts/bench_bwd.py --variant asa_gt > $P/bench_bwd_wan_asa_gt.json 2>&1
+python scripts/bench_bwd.py --workload cog --variant asa_gt > $P/bench_bwd_cog_asa_gt.json 2>&1
+timeout 900 python scripts/sweep.py > $P/sweep_wan.jsonl 2> $P/sweep_wan.err
+timeout 600 python scripts/sweep.py --workload cog > $P/sweep_cog.jsonl 2> $P/sweep_cog.err
 B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-extra"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $P/launches_wan.csv $B > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $P/launches_cog.csv $B --workload cog > /dev/null 2>&1
