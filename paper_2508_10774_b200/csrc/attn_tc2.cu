@@ -125,7 +125,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifdef BLADE_ATTN2_EMU_MASK
 constexpr uint32_t kEmuMask2_64 = BLADE_ATTN2_EMU_MASK, kEmuMask2_128 = BLADE_ATTN2_EMU_MASK;
 #else
-constexpr uint32_t kEmuMask2_64 = 0x01, kEmuMask2_128 = 0x00;
+// d = 64: the pattern of attn_tc2p.cu (pairs 1 and 5 of every 8), so the two
+// kernels stay bit-identical
+constexpr uint32_t kEmuMask2_64 = 0x22, kEmuMask2_128 = 0x00;
 #endif
 
 // Interleaved consumption order of the two blocks' items: A0 B0 A1 B1 ...

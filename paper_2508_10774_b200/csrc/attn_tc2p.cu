@@ -79,9 +79,11 @@ struct CfgP {
 #define BLADE_ATTN2P_QPREFETCH 1  // L2 prefetch of the next item's Q while its slot drains
 #endif
 constexpr float kRescaleThresholdP = 8.0f;  // log2 units
-// exponential pairs on the FMA pipe (as attn_tc2.cu): 1 in 8 for d = 64
+// exponential pairs on the FMA pipe (as attn_tc2.cu), d = 64: pairs 1 and 5 of
+// every 8 (with P in its own columns; Cog attention 0.891 vs 0.917 ms for 0x01,
+// 0.998 for none, 0.894 for 0x11, 0.96 for 3 in 8, 1.02 for 0x55)
 #ifndef BLADE_ATTN2P_EMU64
-#define BLADE_ATTN2P_EMU64 0x01
+#define BLADE_ATTN2P_EMU64 0x22
 #endif
 #ifndef BLADE_ATTN2P_EMU128
 #define BLADE_ATTN2P_EMU128 0x00
