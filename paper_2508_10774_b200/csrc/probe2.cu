@@ -64,7 +64,10 @@ constexpr int kWarpMma2 = kSW, kWarpTma2 = kSW + 1;
 constexpr int kP2Threads = 32 * (kSW + 2);
 
 #ifndef BLADE_PROBE_EMU
-#define BLADE_PROBE_EMU 0x00  // which of every 8 exponential pairs run on the FMA pipe
+// which of every 8 exponential pairs run on the FMA pipe: pair 1 (keep-ratio
+// mask, L2 flushed: Wan 0.165 vs 0.169 ms, Cog 0.179 vs 0.187 ms; 0x01 0.167 /
+// 0.182, 0x10, 0x11, 0x22 0.167-0.169 / 0.183)
+#define BLADE_PROBE_EMU 0x02
 #endif
 constexpr uint32_t kEmu = BLADE_PROBE_EMU;
 
