@@ -36,6 +36,12 @@ using attn::DefaultScale;
 using attn::ex2_poly2;
 using attn::GtArgs;
 
+#ifndef BLADE_ATTN2P_RK64
+#define BLADE_ATTN2P_RK64 6  // d = 64 K / V ring slots (16 KB each)
+#endif
+#ifndef BLADE_ATTN2P_RV64
+#define BLADE_ATTN2P_RV64 6
+#endif
 #ifndef BLADE_ATTN2P_PCHUNK
 #define BLADE_ATTN2P_PCHUNK 1  // d = 128: P handed over in 1, 2 or 4 key chunks
 #endif
@@ -50,8 +56,8 @@ struct CfgP {
   static constexpr int kTile = 128 * D * 2;  // one Q / K / V tile
   static constexpr int kPanels = D / 64;     // 128-byte SW128 panels along d
   static constexpr int kPanel = 128 * 128;
-  static constexpr int kRingK = D == 128 ? 3 : 6;
-  static constexpr int kRingV = D == 128 ? 2 : 6;
+  static constexpr int kRingK = D == 128 ? 3 : BLADE_ATTN2P_RK64;
+  static constexpr int kRingV = D == 128 ? 2 : BLADE_ATTN2P_RV64;
   static constexpr int kOffQ = 0;  // Q_A, Q_B
   static constexpr int kOffRingK = 2 * kTile;
   static constexpr int kOffRingV = kOffRingK + kRingK * kTile;
