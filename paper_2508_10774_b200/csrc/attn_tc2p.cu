@@ -85,11 +85,11 @@ struct CfgP {
 #define BLADE_ATTN2P_QPREFETCH 1  // L2 prefetch of the next item's Q while its slot drains
 #endif
 constexpr float kRescaleThresholdP = 8.0f;  // log2 units
-// exponential pairs on the FMA pipe (as attn_tc2.cu), d = 64: pairs 1 and 5 of
-// every 8 (with P in its own columns; Cog attention 0.891 vs 0.917 ms for 0x01,
+// exponential pairs on the FMA pipe (bit e of the mask: pair e of each 16-pair
+// chunk of a row; as attn_tc2.cu), d = 64: pairs 1 and 5 of every 8 (with P in its own columns; Cog attention 0.891 vs 0.917 ms for 0x01,
 // 0.998 for none, 0.894 for 0x11, 0.96 for 3 in 8, 1.02 for 0x55)
 #ifndef BLADE_ATTN2P_EMU64
-#define BLADE_ATTN2P_EMU64 0x22
+#define BLADE_ATTN2P_EMU64 0x2222
 #endif
 #ifndef BLADE_ATTN2P_EMU128
 #define BLADE_ATTN2P_EMU128 0x00
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           for (int e = 0; e < 16; ++e) {
             const float2 x = fma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sl2, nm);
             float2 pp;
-            if (((D == 64 ? kEmuMaskP64 : kEmuMaskP128) >> (e & 7)) & 1) {
+            if (((D == 64 ? kEmuMaskP64 : kEmuMaskP128) >> (e & 15)) & 1) {
               pp = ex2_poly2(x);
             } else {
               pp.x = ex2(x.x);
