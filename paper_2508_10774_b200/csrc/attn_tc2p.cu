@@ -371,6 +371,11 @@ __global__ void __launch_bounds__(kThreadsP, 1)
             }
           }
         }
+        // kSepP: consume the read-out of each block's last S (every mbarrier
+        // phase that completes has a waiter)
+        if (C::kSepP)
+          for (int t = 0; t < 2; ++t)
+            if (gs[t] > 0) tc::mbar_wait(bar_sf + t, (gs[t] - 1) & 1);
       }
     }
   } else {
