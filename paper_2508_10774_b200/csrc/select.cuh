@@ -21,6 +21,10 @@
 
 #include "common.cuh"
 
+#ifndef BLADE_SEL_TOPK
+#define BLADE_SEL_TOPK 1  // keep-ratio rows by a bitwise top-m search instead of a sort
+#endif
+
 namespace blade {
 
 BLADE_DEVINL bool sel_before(double va, int ia, double vb, int ib) {
@@ -197,9 +201,115 @@ struct RowSelect {
 // network is pure integer compare/select; p~ is formed only after sorting.
 template <int E>
 struct RowSelectF32 {
+  // Keep-ratio mode (lo == hi = m): the top m blocks need no cumulative sums
+  // (the clamp fixes the count), so instead of sorting, the m-th largest
+  // value is found by a bitwise search over the fp32 bits (non-negative
+  // floats order like their bit patterns), ties at it taken by ascending id:
+  // the same set, flag and output as the sort path below.
+  __device__ static bool topk(const float* vals, int Nb, int m, double guard, bool want_flag,
+                              uint8_t* mask_row, int32_t* kv_idx_row, int32_t* kv_cnt_out,
+                              uint32_t* keep_bits) {
+    const int lane = threadIdx.x & 31;
+    uint32_t u[E];
+    double z = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int x = lane * E + e;
+      const float pv = x < Nb ? vals[x] : 0.f;
+      z += double(pv);
+      u[e] = __float_as_uint(pv);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    auto count_ge = [&](uint32_t c) {
+      int n = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) n += (lane * E + e < Nb && u[e] >= c) ? 1 : 0;
+      return int(__reduce_add_sync(0xffffffffu, uint32_t(n)));
+    };
+    // T = the m-th largest value: the largest bit pattern with >= m values at or above it
+    uint32_t T = 0u;
+    for (int b = 31; b >= 0; --b) {
+      const uint32_t c = T | (1u << b);
+      if (count_ge(c) >= m) T = c;
+    }
+    const int g = T == 0xffffffffu ? 0 : count_ge(T + 1u);  // strictly above T
+    const int need = m - g;                                  // ties at T to keep, by id
+    int nt = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) nt += (lane * E + e < Nb && u[e] == T) ? 1 : 0;
+    int pre = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    pre -= nt;  // ties at T in lower lanes (lower ids)
+    bool flag = false;
+    if (want_flag && m < Nb) {
+      // p_(m) = T; p_(m+1) = T again when more than m values reach T, else the
+      // largest value below T (the sort path's pm - pn <= guard pm on p~ = P / Z)
+      uint32_t below = 0u;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (lane * E + e < Nb && u[e] < T) below = below > u[e] ? below : u[e];
+      below = __reduce_max_sync(0xffffffffu, below);
+      const bool tie = g + nt_total(nt) > m;
+      const double inv_z = 1.0 / z;
+      const double pm = double(__uint_as_float(T)) * inv_z;
+      const double pn = double(__uint_as_float(tie ? T : below)) * inv_z;
+      flag = pm - pn <= guard * pm;
+    }
+    const int nwords = (Nb + 31) >> 5;
+    if (lane < 16) keep_bits[lane] = 0u;
+    __syncwarp();
+    int r = pre;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int x = lane * E + e;
+      if (x < Nb) {
+        bool keep = u[e] > T;
+        if (u[e] == T) keep = r++ < need;
+        if (keep) atomicOr(&keep_bits[x >> 5], 1u << (x & 31));
+      }
+    }
+    __syncwarp();
+    const uint32_t myw = lane < nwords ? keep_bits[lane] : 0u;
+    const int cntw = __popc(myw);
+    int wp = cntw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wp, o);
+      if (lane >= o) wp += y;
+    }
+    wp -= cntw;
+    {
+      uint32_t w = myw;
+      int pos = wp;
+      while (w) {
+        const int b = __ffs(w) - 1;
+        w &= w - 1;
+        kv_idx_row[pos++] = lane * 32 + b;
+      }
+    }
+    for (int rr = m + lane; rr < Nb; rr += 32) kv_idx_row[rr] = -1;
+    if (mask_row)
+      for (int j = lane; j < Nb; j += 32) mask_row[j] = (keep_bits[j >> 5] >> (j & 31)) & 1u;
+    if (lane == 0) *kv_cnt_out = m;
+    __syncwarp();
+    return flag;
+  }
+  __device__ static int nt_total(int nt) {
+    return int(__reduce_add_sync(0xffffffffu, uint32_t(nt)));
+  }
+
   __device__ static bool run(const float* vals, int Nb, double tau, int lo, int hi, double guard,
                              bool want_flag, uint8_t* mask_row, int32_t* kv_idx_row,
                              int32_t* kv_cnt_out, uint32_t* keep_bits) {
+#if BLADE_SEL_TOPK
+    if (lo == hi)
+      return topk(vals, Nb, lo, guard, want_flag, mask_row, kv_idx_row, kv_cnt_out, keep_bits);
+#endif
     const int lane = threadIdx.x & 31;
     uint64_t key[E];
     double z = 0.0;
